@@ -1,0 +1,557 @@
+"""Benchmark of the B200 SALR linear hot path (driver contract: see DESIGN.md
+"Measurement").
+
+Workload (one "step"): one decode token-batch (M tokens, default 32) through
+the Llama3-8B SALR linear stack -- 32 layers x 7 linears (q, k, v, o, gate, up,
+down; BASELINE configs[1] shapes, stacked as in configs[3]) at 50% magnitude
+sparsity with LoRA r16 + residual r16 adapters fused (R = 32).  Weights are
+synthetic random-init (no checkpoints offline).  At --gpus N the stack is
+column-sharded: every rank decodes only its 128-column-aligned stripe of each
+linear and the shards are all-gathered (NCCL) at the four layer boundaries
+(after q|k|v, o, gate|up, down) -- SURVEY.md 8(e).
+
+Output: one JSON line (rank 0) with value = whole-job tokens/s (device-timed,
+CUDA events, max over ranks), e2e (host buffers in and out, public API),
+roofline of the dominant kernel (compressed bytes / kernel time vs the
+measured HBM copy bandwidth), cuBLAS dense-bf16 comparator, clocks (NVML
+sampled during the timed region), and the CPU baseline (oracle port of the
+reference pipelined_forward on the host cores, bounded sample).
+
+``--impl reference`` times the reference's CPU algorithm instead (the oracle
+port in oracle/salr_oracle.py; the reference package itself is pure Python
+and cannot travel to the GPU box) on the same workload and prints the same
+metric with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+LINEARS = ["q", "k", "v", "o", "gate", "up", "down"]
+SHAPES = {"q": (4096, 4096), "k": (4096, 1024), "v": (4096, 1024), "o": (4096, 4096),
+          "gate": (4096, 14336), "up": (4096, 14336), "down": (14336, 4096)}
+METRIC = "SALR linear tokens/s & compressed-weight HBM GB/s, Llama3-8B shapes @50% sparsity"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["salr", "reference"], default="salr")
+    ap.add_argument("--tokens", type=int, default=32)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--sparsity", type=float, default=0.5)
+    ap.add_argument("--batches", default="1,8,32", help="extra decode batch sizes reported per-M")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cublas", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks: NVML sampled in a background thread during the timed region
+
+class ClockSampler:
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    _REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                break
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        reasons = sorted(self.reasons - {"gpu_idle"})
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# distributed helpers
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def shard_cols(n: int, world: int, rank: int):
+    """128-column-aligned stripe of an output dimension."""
+    tiles = (n + 127) // 128
+    t0 = tiles * rank // world
+    t1 = tiles * (rank + 1) // world
+    return min(128 * t0, n), min(128 * t1, n)
+
+
+# ---------------------------------------------------------------------------
+# reference arm: oracle (CPU) on a bounded sample
+
+def cpu_sample(tokens: int, sparsity: float, budget_s: float = 20.0):
+    """Time the oracle port of the reference pipelined_forward (f64, the
+    reference's 64x8-byte tile order) on one layer's 7 linears."""
+    import numpy as np
+    import torch
+    from oracle import salr_oracle as O
+    from paper_2601_16991_b200 import synthetic
+
+    try:
+        from threadpoolctl import threadpool_info
+        blas_threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+    except Exception:
+        blas_threads = os.cpu_count()
+    rng = np.random.default_rng(0)
+    x = synthetic.gen_x(tokens, 14336, seed=7).double().numpy()
+    linears = {}
+    for i, name in enumerate(LINEARS):
+        k, n = SHAPES[name]
+        w = synthetic.gen_weight(k, n, 1000 + i).double().numpy()
+        thr = 0.02 * 0.6744897501960817  # |w| quantile for N(0, 0.02^2) at 50%
+        w[np.abs(w) < thr * (sparsity / 0.5 if sparsity != 0.5 else 1.0)] = 0.0
+        s = O.encode(w)
+        ads = [O.Adapter(rng.normal(size=(k, 16)) / 64, rng.normal(size=(16, n)) * 0.02, 16),
+               O.Adapter(rng.normal(size=(k, 16)) / 64, rng.normal(size=(16, n)) * 0.02, 16, 2.0)]
+        linears[name] = (s, O.fuse(ads), k)
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        for name in LINEARS:
+            s, f, k = linears[name]
+            O.pipelined_forward(x[:, :k], s, f)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget_s or len(times) >= 3:
+            break
+    layer_s = statistics.median(times)
+    step_s = layer_s * 32
+    comp = sum(linears[nm][0].rows * linears[nm][0].bytes_per_row + 4 * linears[nm][0].nnz for nm in LINEARS)
+    return {
+        "value": tokens / step_s, "unit": "tokens/s", "cores": blas_threads, "kind": "port",
+        "sample": f"oracle pipelined_forward (f64, 64x8-byte tiles, serial) over one layer's 7 linears at "
+                  f"M={tokens}, median of {len(times)} passes = {layer_s:.3f} s/layer, x32 layers extrapolated; "
+                  f"{os.cpu_count()} host cores visible, OpenBLAS threads={blas_threads}",
+        "compressed_gbs": comp * 32 / step_s / 1e9,
+        "layer_s": layer_s,
+    }
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    res = cpu_sample(args.tokens, args.sparsity)
+    steps_s = []
+    for _ in range(max(1, min(args.steps, 1))):
+        steps_s.append(32 * res["layer_s"])
+    ms = 1e3 * statistics.median(steps_s)
+    line = {
+        "metric": METRIC, "impl": "reference", "value": res["value"], "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "llama3-8b 32-layer SALR linear stack, decode batch", "tokens": args.tokens,
+                   "layers": 32, "sparsity": args.sparsity, "adapters": "r16+r16"},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "compressed_gbs": res["compressed_gbs"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the B200 arm
+
+def build_stack(layers, world, rank, sparsity, device):
+    """Per layer: {name: (BitmapSparseMatrix shard, FusedAdapters shard, (k, n_local), col range)}."""
+    import torch
+    import paper_2601_16991_b200 as S
+
+    g = torch.Generator(device=device).manual_seed(1234 + 17 * rank)
+    thr = 0.02 * 0.6744897501960817  # N(0, 0.02^2) |w| median: prunes 50% by magnitude
+    q = {0.3: 0.3853204664075676, 0.5: 0.6744897501960817, 0.7: 1.0364333894937898}.get(sparsity)
+    if q is None:
+        raise SystemExit(f"unsupported sparsity {sparsity}")
+    thr = 0.02 * q
+    stack = []
+    for layer in range(layers):
+        lin = {}
+        for name in LINEARS:
+            k, n = SHAPES[name]
+            c0, c1 = shard_cols(n, world, rank)
+            nl = c1 - c0
+            w = (torch.randn(k, nl, generator=g, device=device) * 0.02).to(torch.bfloat16)
+            w = torch.where(w.float().abs() < thr, torch.zeros_like(w), w)
+            s = S.encode(w, value_dtype="bf16")
+            del w
+            ads = [S.AdapterPair((torch.randn(k, 16, generator=g, device=device) / 64).bfloat16().float(),
+                                 (torch.randn(16, nl, generator=g, device=device) * 0.02).bfloat16().float(), 16),
+                   S.AdapterPair((torch.randn(k, 16, generator=g, device=device) / 64).bfloat16().float(),
+                                 (torch.randn(16, nl, generator=g, device=device) * 0.02).bfloat16().float(), 16, 2.0)]
+            fused = S.fuse(ads)
+            fused.device_operands()
+            lin[name] = (s, fused, (k, nl), (c0, c1))
+        stack.append(lin)
+    return stack
+
+
+class StackRunner:
+    """One decode step through the (sharded) stack; all device work on one stream."""
+
+    def __init__(self, stack, tokens, world, out_dtype, group=None):
+        import torch
+        import paper_2601_16991_b200 as S
+        self.S, self.stack, self.M, self.world, self.group = S, stack, tokens, world, group
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.x_in = torch.zeros(tokens, 4096, dtype=torch.bfloat16, device=dev)
+        self.bufs = {}
+        for name in LINEARS:
+            k, n = SHAPES[name]
+            nl = stack[0][name][2][1]
+            self.bufs[name] = torch.empty(tokens, nl, dtype=torch.bfloat16, device=dev)
+        self.full = {w: torch.empty(tokens, w, dtype=torch.bfloat16, device=dev) for w in (4096, 14336, 6144, 28672)}
+        self.launches_per_step = 0
+
+    def _gather(self, locals_, widths):
+        """All-gather column shards of one or more linears into full rows."""
+        import torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return locals_
+        out = []
+        for t, w in zip(locals_, widths):
+            g = torch.empty(self.world, *t.shape, dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(g, t.contiguous(), group=self.group)
+            # rank-major shards -> full columns (shards are 128-col stripes in rank order)
+            out.append(g.permute(1, 0, 2).reshape(t.shape[0], -1)[:, :w])
+        return out
+
+    def step(self, x):
+        S = self.S
+        h = x
+        launches = 0
+        for lin in self.stack:
+            outs = {}
+            for name in ("q", "k", "v"):
+                s, f, _, _ = lin[name]
+                outs[name] = S.salr_linear(h, s, f, out=self.bufs[name], check_finite=False)
+                launches += 2
+            q, _, _ = self._gather([outs["q"], outs["k"], outs["v"]], [4096, 1024, 1024])
+            s, f, _, _ = lin["o"]
+            o = S.salr_linear(q, s, f, out=self.bufs["o"], check_finite=False)
+            launches += 2
+            (o,) = self._gather([o], [4096])
+            for name in ("gate", "up"):
+                s, f, _, _ = lin[name]
+                outs[name] = S.salr_linear(o, s, f, out=self.bufs[name], check_finite=False)
+                launches += 2
+            # the stack is linears only (the MLP nonlinearity is outside the hot
+            # path): down consumes the gathered gate projection
+            gate, _ = self._gather([outs["gate"], outs["up"]], [14336, 14336])
+            s, f, _, _ = lin["down"]
+            d = S.salr_linear(gate, s, f, out=self.bufs["down"], check_finite=False)
+            launches += 2
+            (h,) = self._gather([d], [4096])
+        self.launches_per_step = launches
+        return h
+
+
+def time_steps(fn, steps, warmup, world, sampler_dev):
+    import torch
+    import torch.distributed as dist
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(sampler_dev) as cs:
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        e1.synchronize()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    return ms, cs.summary()
+
+
+def per_linear_kernel_times(stack, tokens, reps=20):
+    """Average device time of each linear's launch (U pre-kernel + fused kernel),
+    CUDA events on the launching stream, layers rotated to defeat L2."""
+    import torch
+    import paper_2601_16991_b200 as S
+    res = {}
+    x = {4096: torch.randn(tokens, 4096, device="cuda").bfloat16(),
+         14336: torch.randn(tokens, 14336, device="cuda").bfloat16()}
+    for name in LINEARS:
+        k, nl = stack[0][name][2]
+        out = torch.empty(tokens, nl, dtype=torch.bfloat16, device="cuda")
+        L = len(stack)
+        for i in range(3):
+            s, f, _, _ = stack[i % L][name]
+            S.salr_linear(x[k], s, f, out=out, check_finite=False)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(reps):
+            s, f, _, _ = stack[i % L][name]
+            S.salr_linear(x[k], s, f, out=out, check_finite=False)
+        e1.record()
+        e1.synchronize()
+        s0 = stack[0][name][0]
+        res[name] = {"us": 1e3 * e0.elapsed_time(e1) / reps, "compressed_bytes": s0.compressed_bytes,
+                     "nnz": s0.nnz, "shape": [k, nl]}
+    return res
+
+
+def cublas_times(stack, tokens, reps=20):
+    """cuBLAS dense bf16 baseline: X @ W_merged (W_hat + A B densified), same rotation."""
+    import torch
+    import paper_2601_16991_b200 as S
+    res = {}
+    L = min(len(stack), 8)
+    for name in LINEARS:
+        k, nl = stack[0][name][2]
+        ws = []
+        for i in range(L):
+            s, f, _, _ = stack[i][name]
+            ws.append((S.decode(s) + f.a_cat @ f.b_cat).bfloat16())
+        x = torch.randn(tokens, k, device="cuda").bfloat16()
+        for i in range(3):
+            torch.matmul(x, ws[i % L])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(reps):
+            torch.matmul(x, ws[i % L])
+        e1.record()
+        e1.synchronize()
+        res[name] = {"us": 1e3 * e0.elapsed_time(e1) / reps, "dense_bytes": 2 * k * nl}
+        del ws
+        torch.cuda.empty_cache()
+    return res
+
+
+def run_salr(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_setup(args)
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    hbm_peak, tf_peak, peak_src = peaks()
+    t_setup = time.time()
+    stack = build_stack(args.layers, world, rank, args.sparsity, dev)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t_setup
+    M = args.tokens
+
+    # ---- device-timed steps (graph-captured stack)
+    runner = StackRunner(stack, M, world, torch.bfloat16)
+    x0 = torch.randn(M, 4096, device=dev).bfloat16()
+    runner.x_in.copy_(x0)
+    use_graph = world == 1
+    if use_graph:
+        runner.step(runner.x_in)  # compile-free warm call; allocates workspaces
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            out_static = runner.step(runner.x_in)
+        step_fn = graph.replay
+    else:
+        step_fn = lambda: runner.step(runner.x_in)  # noqa: E731
+    ms, clocks = time_steps(step_fn, args.steps, args.warmup, world, local)
+    ms_per_step = ms / args.steps
+    tokens_per_s = M / (ms_per_step / 1e3)  # every rank processes the same M tokens (sharded columns)
+
+    comp_bytes_local = sum(lin[n][0].compressed_bytes for lin in stack for n in LINEARS)
+    comp_bytes = comp_bytes_local
+    if world > 1:
+        t = torch.tensor([float(comp_bytes_local)], device=dev)
+        dist.all_reduce(t)
+        comp_bytes = t.item()
+
+    # ---- e2e: pinned host X in, host Y out, every step
+    h_x = torch.empty(M, 4096, dtype=torch.bfloat16, pin_memory=True)
+    h_x.copy_(x0.cpu())
+    h_y = torch.empty(M, 4096, dtype=torch.bfloat16, pin_memory=True)
+
+    def e2e_step():
+        runner.x_in.copy_(h_x, non_blocking=True)
+        if use_graph:
+            graph.replay()
+            y = out_static
+        else:
+            y = runner.step(runner.x_in)
+        h_y.copy_(y, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    e2e_steps = max(5, min(args.steps, 50))
+    for _ in range(3):
+        e2e_step()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = t.item()
+    e2e_value = M * e2e_steps / e2e_s
+
+    line = None
+    if rank == 0:
+        per = per_linear_kernel_times(stack, M)
+        k_bytes = sum(v["compressed_bytes"] for v in per.values())
+        k_us = sum(v["us"] for v in per.values())
+        achieved = k_bytes / (k_us * 1e-6) / 1e9
+        traffic = None
+        prof = os.path.join(REPO, "profiles", "ncu_summary.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("traffic_bytes_per_launch")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                "kernel": "salr_linear_kernel (+ adapter_u_kernel, PDL-overlapped)",
+                "algorithmic_bytes": "K*ceil(N/8) + 2*nnz per linear (SURVEY.md 8(d))",
+                "per_linear": per}
+        extra = {}
+        if not args.no_cublas and world == 1:
+            cb = cublas_times(stack, M)
+            cb_us = sum(v["us"] for v in cb.values())
+            extra["cublas_dense_bf16"] = {"us_per_layer": cb_us, "salr_us_per_layer": k_us,
+                                          "speedup": cb_us / k_us, "per_linear": cb}
+        per_m = {}
+        if world == 1:
+            for mb in [int(v) for v in args.batches.split(",") if v]:
+                if mb == M:
+                    per_m[str(mb)] = {"tokens_per_s": tokens_per_s, "ms_per_step": ms_per_step}
+                    continue
+                r2 = StackRunner(stack, mb, 1, torch.bfloat16)
+                r2.x_in.copy_(torch.randn(mb, 4096, device=dev).bfloat16())
+                r2.step(r2.x_in)
+                torch.cuda.synchronize()
+                g2 = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g2):
+                    r2.step(r2.x_in)
+                ms2, _ = time_steps(g2.replay, max(5, args.steps // 2), 3, 1, local)
+                per_m[str(mb)] = {"tokens_per_s": mb / (ms2 / max(5, args.steps // 2) / 1e3),
+                                  "ms_per_step": ms2 / max(5, args.steps // 2),
+                                  "compressed_gbs": comp_bytes / (ms2 / max(5, args.steps // 2) / 1e3) / 1e9}
+                del g2, r2
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            c = cpu_sample(M, args.sparsity)
+            cpu = {k: c[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        line = {
+            "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic random-init weights/inputs",
+            "config": {"workload": "llama3-8b 32-layer SALR linear stack (q,k,v,o,gate,up,down; configs[1] "
+                                   "shapes x32 layers = configs[3] at this N), one decode token-batch per step",
+                       "tokens": M, "layers": args.layers, "sparsity": args.sparsity, "adapters": "r16+r16 fused (R=32)",
+                       "parallelism": f"col-shard{world}" if world > 1 else "single",
+                       "l2": "working set 7.85 GB >> 126 MB L2 (inputs larger than L2)",
+                       "graph": "CUDA graph per step" if use_graph else "eager (NCCL all-gathers)"},
+            "compressed_gbs": comp_bytes / (ms_per_step / 1e3) / 1e9,
+            "compressed_bytes_per_step": comp_bytes,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": int(h_x.numel() * 2),
+                    "d2h_bytes_per_step": int(h_y.numel() * 2),
+                    "how": "pinned host X -> device, stack forward (public salr_linear API, graph-replayed), "
+                           "device Y -> pinned host, synchronize; wall clock"},
+            "gpu_launches": runner.launches_per_step * args.steps,
+            "clocks": clocks,
+            "per_batch": per_m,
+            "setup_s": setup_s,
+            **extra,
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_salr(args)
+
+
+if __name__ == "__main__":
+    main()

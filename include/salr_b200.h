@@ -1,0 +1,130 @@
+/*
+ * salr_b200.h -- C ABI of the B200-native SALR linear hot path.
+ *
+ * Drop-in boundary for the reference package's hot path (reference
+ * pkg/src/salr/__init__.py:61-82 re-exports; there is no FFI in the
+ * reference, so these entry points are what its Python API binds to through
+ * ctypes -- see INTEGRATION.md).  Every entry point:
+ *   - takes plain device pointers, sizes and a cudaStream_t (as void*);
+ *   - is stream-ordered and CUDA-graph capturable;
+ *   - never allocates device memory (workspaces come from the caller);
+ *   - returns an int status that maps 1:1 onto the reference error tree
+ *     (reference pkg/src/salr/errors.py:22-51).
+ *
+ * Matrix orientation follows the reference: a weight W is (rows=d_in=K,
+ * cols=d_out=N) and the linear computes y = x @ W (reference
+ * fusion.py:109-130, pipeline.py:405-461).
+ *
+ * TB ("tiled bitmap") device format -- the GPU-resident form of
+ * BitmapSparseMatrix (reference bitmap.py:88-143):
+ *   tiles of 64 rows x 128 cols, tile t = nt * n_kt + kt;
+ *   record(t) at byte offset 16 * tile_off[t]:
+ *     u32 hdr[4]        group value offsets G1, G2, G3 and tile nnz
+ *     u32 bits[4][64]   bits[g][k] bit l  <=> element (k, 32 g + l)
+ *     values            group-major, then row-major set-bit order
+ *     zero pad to 16 B
+ *   The logical bitmap is bit-identical to the reference's (LSB-first, bit
+ *   t of byte b = column 8b+t, reference bitmap.py:4-6); salr_to_reference
+ *   reproduces the reference row-major bitmap and value order exactly.
+ */
+#ifndef SALR_B200_H
+#define SALR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> reference exceptions (errors.py:22-51) */
+#define SALR_OK 0
+#define SALR_ERR_SHAPE 1      /* ShapeError      */
+#define SALR_ERR_DOMAIN 2     /* DomainError     */
+#define SALR_ERR_BOUNDS 3     /* BoundsError     */
+#define SALR_ERR_CONFIG 4     /* ConfigError     */
+#define SALR_ERR_FORMAT 5     /* FormatError     */
+#define SALR_ERR_CORRUPTION 6 /* CorruptionError */
+#define SALR_ERR_CUDA 7       /* SalrError (device/runtime failure) */
+
+/* element types */
+#define SALR_F32 0
+#define SALR_BF16 1
+#define SALR_F64 2
+
+#define SALR_TILE_K 64
+#define SALR_TILE_N 128
+
+/* ---- library ------------------------------------------------------------ */
+int salr_version(void);
+/* Message for the last non-OK status returned on this thread. */
+const char* salr_last_error(void);
+
+/* ---- geometry ------------------------------------------------------------ */
+/* Tile grid of a rows x cols matrix.  Replaces bitmap.bytes_per_row /
+ * BitmapSparseMatrix shape bookkeeping (reference bitmap.py:146-147). */
+int salr_tb_geometry(int64_t rows, int64_t cols, int64_t* n_kt, int64_t* n_nt, int64_t* n_tiles);
+
+/* ---- encode (reference bitmap.py:150-165) -------------------------------- */
+/* Phase 1: count set bits per tile/group and write tile_off[n_tiles + 1]
+ * (16-byte units).  tile_cnt is a caller workspace of 4 * n_tiles u32.  The
+ * caller reads tile_off[n_tiles] to size the record buffer. */
+int salr_encode_count(const void* dense, int in_dtype, int64_t rows, int64_t cols, int64_t ld,
+                      int value_dtype, uint32_t* tile_cnt, uint32_t* tile_off, void* stream);
+/* Phase 2: write the records (bitmap words + compacted values). */
+int salr_encode_write(const void* dense, int in_dtype, int64_t rows, int64_t cols, int64_t ld,
+                      int value_dtype, const uint32_t* tile_cnt, const uint32_t* tile_off,
+                      uint8_t* records, void* stream);
+
+/* ---- decode (reference bitmap.py:168-212: decode / decode_block) --------- */
+/* Dense window rows [r0,r1) x cols [c0,c1) into out (row-major, ld_out). */
+int salr_decode(const uint8_t* records, const uint32_t* tile_off, int value_dtype, int64_t rows,
+                int64_t cols, int64_t r0, int64_t r1, int64_t c0, int64_t c1, void* out,
+                int out_dtype, int64_t ld_out, void* stream);
+
+/* nnz of the whole matrix (sum of record headers) -> *nnz_dev (u64, device). */
+int salr_tb_nnz(const uint8_t* records, const uint32_t* tile_off, int64_t n_tiles,
+                unsigned long long* nnz_dev, void* stream);
+
+/* ---- reference layout <-> TB (reference bitmap.py:88-143 storage) -------- */
+/* rowtile_off: workspace of rows * n_nt + 1 u32 (exclusive value offsets). */
+int salr_to_reference(const uint8_t* records, const uint32_t* tile_off, int value_dtype, int64_t rows,
+                      int64_t cols, uint32_t* rowtile_off, uint8_t* bitmap_out, void* values_out,
+                      int values_dtype, void* stream);
+/* Phase 1: from a reference row-major bitmap (rows x ceil(cols/8) u8),
+ * compute rowtile_off (rows*n_nt+1), tile_cnt (4*n_tiles) and tile_off. */
+int salr_from_reference_count(const uint8_t* bitmap, int64_t rows, int64_t cols, int value_dtype,
+                              uint32_t* rowtile_off, uint32_t* tile_cnt, uint32_t* tile_off,
+                              void* stream);
+/* Phase 2: write TB records from the reference bitmap + values. */
+int salr_from_reference_write(const uint8_t* bitmap, const void* values, int values_dtype,
+                              int64_t rows, int64_t cols, int value_dtype,
+                              const uint32_t* rowtile_off, const uint32_t* tile_cnt,
+                              const uint32_t* tile_off, uint8_t* records, void* stream);
+
+/* ---- SALR linear forward (reference pipeline.py:405-461, fusion.py:87-130) */
+/* Y (M x N) = X (M x K) @ decode(W) + (X @ A_cat) @ B_cat.
+ *   x      bf16, row-major, leading dim ldx (ldx % 8 == 0, 16-byte aligned)
+ *   acat   bf16 K x r_pad row-major (zero-padded rank columns) or NULL
+ *   bcat_t bf16 (n_nt*128) x r_pad row-major = B_cat^T, zero padded, or NULL
+ *   r_pad  64 (the fused rank R = sum r_i must be <= 64) or 0 without adapters
+ *   y      f32 or bf16, row-major, leading dim ldy
+ *   stages    shared-memory ring slots (PipelineConfig.ring_capacity;
+ *             1 = serial decode/MMA schedule, <= 0 = deepest that fits)
+ *   num_ctas  persistent CTAs (<= 0: one per SM)
+ *   workspace >= salr_linear_workspace_bytes(M, N, K, r_pad, num_ctas); its
+ *   first 256 KiB (ticket counters at fixed offsets) must be zeroed once at
+ *   allocation -- the kernels leave the counters zero
+ *   on exit, so the same workspace serves back-to-back / graph-replayed
+ *   calls.  Split-K partials are summed in a fixed order: results are
+ *   bit-identical from run to run for a given num_ctas. */
+size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pad, int num_ctas);
+int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const uint8_t* records,
+                        const uint32_t* tile_off, int64_t N, const void* acat, const void* bcat_t,
+                        int64_t r_pad, void* y, int y_dtype, int64_t ldy, void* workspace,
+                        size_t workspace_bytes, int stages, int num_ctas, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SALR_B200_H */

@@ -1,0 +1,515 @@
+// Bitmap codec kernels for the TB tile format: encode (two-pass, warp-ballot /
+// popc prefix offsets), decode / decode-window, and bit-exact conversion to
+// and from the reference's row-major bitmap + value layout.
+//
+// Reference semantics restated here:
+//   encode        pkg/src/salr/bitmap.py:150-165  (f32 cast, +0.0, != 0 mask,
+//                 LSB-first packing, row-major value order)
+//   decode        pkg/src/salr/bitmap.py:168-180
+//   decode_block  pkg/src/salr/bitmap.py:183-212
+//   storage       pkg/src/salr/bitmap.py:88-143   (bitmap rows x ceil(cols/8))
+#include <cstdint>
+#include <cstring>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "salr_format.cuh"
+#include "salr_status.cuh"
+
+namespace salr {
+
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+// ------------------------------------------------------------------ scans
+// Single-block exclusive scan of n u32 items produced by a functor; writes
+// out[0..n] (out[n] = total).  Used for tile and row-tile offsets (setup-time
+// work; n <= a few million).
+struct TileUnitsFn {
+  const uint32_t* cnt;
+  int vbytes;
+  __device__ uint32_t operator()(int64_t t) const {
+    uint32_t c = cnt[4 * t] + cnt[4 * t + 1] + cnt[4 * t + 2] + cnt[4 * t + 3];
+    return record_units(c, vbytes);
+  }
+};
+struct ArrayFn {
+  const uint32_t* a;
+  __device__ uint32_t operator()(int64_t i) const { return a[i]; }
+};
+
+template <class F>
+__global__ void __launch_bounds__(1024) scan1_kernel(F f, int64_t n, uint32_t* out) {
+  constexpr int kItems = 4;
+  __shared__ uint32_t warp_tot[32];
+  __shared__ uint32_t carry_s;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) carry_s = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += 1024 * kItems) {
+    uint32_t v[kItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      int64_t idx = base + (int64_t)tid * kItems + i;
+      v[i] = idx < n ? f(idx) : 0u;
+      sum += v[i];
+    }
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = warp_tot[lane];
+      uint32_t wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += y;
+      }
+      warp_tot[lane] = wi - w;  // exclusive
+    }
+    __syncthreads();
+    uint32_t run = carry_s + warp_tot[warp] + incl - sum;
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+      int64_t idx = base + (int64_t)tid * kItems + i;
+      if (idx < n) out[idx] = run;
+      run += v[i];
+    }
+    __syncthreads();
+    if (tid == 1023) carry_s = run;
+    __syncthreads();
+  }
+  if (tid == 0) out[n] = carry_s;
+}
+
+// ------------------------------------------------------------------ encode
+// grid = n_tiles, block = 128 (warp g <-> 32-column group g, lane <-> column).
+__global__ void encode_count_kernel(const void* __restrict__ dense, int in_dtype, int64_t rows,
+                                    int64_t cols, int64_t ld, int64_t n_kt,
+                                    uint32_t* __restrict__ tile_cnt) {
+  const int64_t t = blockIdx.x;
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t col = nt * kTileN + 32 * g + lane;
+  uint32_t cnt = 0;
+  for (int k = 0; k < kTileK; ++k) {
+    const int64_t row = kt * kTileK + k;
+    bool keep = false;
+    if (row < rows && col < cols) keep = load_as_f32(dense, in_dtype, row * ld + col) != 0.0f;
+    cnt += __popc(__ballot_sync(0xffffffffu, keep));
+  }
+  if (lane == 0) tile_cnt[4 * t + g] = cnt;
+}
+
+__global__ void encode_write_kernel(const void* __restrict__ dense, int in_dtype, int64_t rows,
+                                    int64_t cols, int64_t ld, int64_t n_kt, int value_dtype,
+                                    const uint32_t* __restrict__ tile_cnt,
+                                    const uint32_t* __restrict__ tile_off,
+                                    uint8_t* __restrict__ records) {
+  const int64_t t = blockIdx.x;
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t col = nt * kTileN + 32 * g + lane;
+  uint8_t* rec = records + 16ull * tile_off[t];
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(rec);
+  uint32_t* bits = hdr + 4;
+  const uint32_t c0 = tile_cnt[4 * t], c1 = tile_cnt[4 * t + 1], c2 = tile_cnt[4 * t + 2],
+                 c3 = tile_cnt[4 * t + 3];
+  const uint32_t gbase[4] = {0u, c0, c0 + c1, c0 + c1 + c2};
+  const uint32_t nnz = c0 + c1 + c2 + c3;
+  if (threadIdx.x == 0) {
+    hdr[0] = gbase[1];
+    hdr[1] = gbase[2];
+    hdr[2] = gbase[3];
+    hdr[3] = nnz;
+  }
+  const uint32_t lt = lanemask_lt();
+  uint32_t off = gbase[g];
+  const int vb = value_bytes(value_dtype);
+  for (int k = 0; k < kTileK; ++k) {
+    const int64_t row = kt * kTileK + k;
+    float f = 0.0f;
+    if (row < rows && col < cols) f = load_as_f32(dense, in_dtype, row * ld + col) + 0.0f;
+    const bool keep = f != 0.0f;
+    const uint32_t word = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) bits[g * kTileK + k] = word;
+    if (keep) {
+      const uint32_t idx = off + __popc(word & lt);
+      if (value_dtype == kBF16)
+        reinterpret_cast<__nv_bfloat16*>(rec + kValOffset)[idx] = __float2bfloat16_rn(f);
+      else
+        reinterpret_cast<float*>(rec + kValOffset)[idx] = f;
+    }
+    off += __popc(word);
+  }
+  // zero the pad bytes up to the 16-byte record boundary
+  if (threadIdx.x < 16) {
+    const uint32_t used = kValOffset + nnz * vb;
+    const uint32_t end = 16u * (tile_off[t + 1] - tile_off[t]);
+    const uint32_t b = used + threadIdx.x;
+    if (b < end) rec[b] = 0;
+  }
+}
+
+// ------------------------------------------------------------------ decode
+__device__ __forceinline__ float tb_value(const uint8_t* rec, int value_dtype, uint32_t idx) {
+  if (value_dtype == kBF16)
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(rec + kValOffset)[idx]);
+  return reinterpret_cast<const float*>(rec + kValOffset)[idx];
+}
+
+__global__ void decode_kernel(const uint8_t* __restrict__ records, const uint32_t* __restrict__ tile_off,
+                              int value_dtype, int64_t n_kt, int64_t r0, int64_t r1, int64_t c0,
+                              int64_t c1, int64_t kt0, int64_t nt0, int64_t kt_span, void* out,
+                              int out_dtype, int64_t ld_out) {
+  const int64_t kt = kt0 + blockIdx.x % kt_span;
+  const int64_t nt = nt0 + blockIdx.x / kt_span;
+  const int64_t t = nt * n_kt + kt;
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t col = nt * kTileN + 32 * g + lane;
+  const uint8_t* rec = records + 16ull * tile_off[t];
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec);
+  const uint32_t* bits = hdr + 4 + g * kTileK;
+  uint32_t off = g == 0 ? 0u : hdr[g - 1];
+  const uint32_t lt = lanemask_lt();
+  const bool col_in = col >= c0 && col < c1;
+  for (int k = 0; k < kTileK; ++k) {
+    const int64_t row = kt * kTileK + k;
+    const uint32_t word = bits[k];
+    if (col_in && row >= r0 && row < r1) {
+      float v = 0.0f;
+      if ((word >> lane) & 1u) v = tb_value(rec, value_dtype, off + __popc(word & lt));
+      const int64_t o = (row - r0) * ld_out + (col - c0);
+      if (out_dtype == kF32) static_cast<float*>(out)[o] = v;
+      else if (out_dtype == kBF16) static_cast<__nv_bfloat16*>(out)[o] = __float2bfloat16_rn(v);
+      else static_cast<double*>(out)[o] = (double)v;
+    }
+    off += __popc(word);
+  }
+}
+
+__global__ void tb_nnz_kernel(const uint8_t* __restrict__ records, const uint32_t* __restrict__ tile_off,
+                              int64_t n_tiles, unsigned long long* nnz) {
+  unsigned long long s = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_tiles;
+       t += (int64_t)gridDim.x * blockDim.x)
+    s += reinterpret_cast<const uint32_t*>(records + 16ull * tile_off[t])[3];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(nnz, s);
+}
+
+// ------------------------------------------------------------------ TB -> reference
+// rowtile_cnt[row * n_nt + nt] = set bits of `row` inside tile column nt.
+__global__ void tb_rowtile_count_kernel(const uint8_t* __restrict__ records,
+                                        const uint32_t* __restrict__ tile_off, int64_t rows,
+                                        int64_t n_kt, int64_t n_nt, uint32_t* __restrict__ cnt) {
+  const int64_t t = blockIdx.x;
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const int k = threadIdx.x;  // 64 threads
+  const int64_t row = kt * kTileK + k;
+  if (row >= rows) return;
+  const uint32_t* bits = reinterpret_cast<const uint32_t*>(records + 16ull * tile_off[t]) + 4;
+  uint32_t c = 0;
+#pragma unroll
+  for (int g = 0; g < kGroups; ++g) c += __popc(bits[g * kTileK + k]);
+  cnt[row * n_nt + nt] = c;
+}
+
+__global__ void tb_to_reference_kernel(const uint8_t* __restrict__ records,
+                                       const uint32_t* __restrict__ tile_off, int value_dtype,
+                                       int64_t rows, int64_t cols, int64_t n_kt, int64_t n_nt,
+                                       const uint32_t* __restrict__ rowtile_off,
+                                       uint8_t* __restrict__ bitmap_out, void* values_out,
+                                       int values_dtype) {
+  const int64_t t = blockIdx.x;
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t bpr = (cols + 7) / 8;
+  const uint8_t* rec = records + 16ull * tile_off[t];
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec);
+  const uint32_t* bits = hdr + 4;
+  uint32_t off = g == 0 ? 0u : hdr[g - 1];
+  const uint32_t lt = lanemask_lt();
+  for (int k = 0; k < kTileK; ++k) {
+    const int64_t row = kt * kTileK + k;
+    const uint32_t word = bits[g * kTileK + k];
+    if (row < rows) {
+      uint32_t before = 0;
+      for (int gg = 0; gg < g; ++gg) before += __popc(bits[gg * kTileK + k]);
+      if ((word >> lane) & 1u) {
+        const float v = tb_value(rec, value_dtype, off + __popc(word & lt));
+        const uint32_t ridx = rowtile_off[row * n_nt + nt] + before + __popc(word & lt);
+        if (values_dtype == kF32) static_cast<float*>(values_out)[ridx] = v;
+        else static_cast<__nv_bfloat16*>(values_out)[ridx] = __float2bfloat16_rn(v);
+      }
+      if (lane < 4) {
+        const int64_t cb = nt * 16 + 4 * g + lane;
+        if (cb < bpr) bitmap_out[row * bpr + cb] = (uint8_t)(word >> (8 * lane));
+      }
+    }
+    off += __popc(word);
+  }
+}
+
+// ------------------------------------------------------------------ reference -> TB
+__device__ __forceinline__ uint32_t ref_word(const uint8_t* __restrict__ bitmap, int64_t bpr,
+                                             int64_t row, int64_t byte0) {
+  uint32_t w = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t b = byte0 + j;
+    if (b < bpr) w |= (uint32_t)bitmap[row * bpr + b] << (8 * j);
+  }
+  return w;
+}
+
+__global__ void ref_rowtile_count_kernel(const uint8_t* __restrict__ bitmap, int64_t rows, int64_t cols,
+                                         int64_t n_nt, uint32_t* __restrict__ cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * n_nt) return;
+  const int64_t row = i / n_nt, nt = i % n_nt;
+  const int64_t bpr = (cols + 7) / 8;
+  uint32_t c = 0;
+#pragma unroll
+  for (int g = 0; g < kGroups; ++g) c += __popc(ref_word(bitmap, bpr, row, nt * 16 + 4 * g));
+  cnt[i] = c;
+}
+
+// tile_cnt[4t+g] from the reference bitmap; one thread per (tile, group).
+__global__ void ref_tile_count_kernel(const uint8_t* __restrict__ bitmap, int64_t rows, int64_t cols,
+                                      int64_t n_kt, int64_t n_tiles, uint32_t* __restrict__ tile_cnt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_tiles * kGroups) return;
+  const int64_t t = i / kGroups;
+  const int g = (int)(i % kGroups);
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const int64_t bpr = (cols + 7) / 8;
+  uint32_t c = 0;
+  for (int k = 0; k < kTileK; ++k) {
+    const int64_t row = kt * kTileK + k;
+    if (row < rows) c += __popc(ref_word(bitmap, bpr, row, nt * 16 + 4 * g));
+  }
+  tile_cnt[i] = c;
+}
+
+__global__ void ref_to_tb_kernel(const uint8_t* __restrict__ bitmap, const void* values, int values_dtype,
+                                 int64_t rows, int64_t cols, int64_t n_kt, int64_t n_nt, int value_dtype,
+                                 const uint32_t* __restrict__ rowtile_off,
+                                 const uint32_t* __restrict__ tile_cnt,
+                                 const uint32_t* __restrict__ tile_off, uint8_t* __restrict__ records) {
+  const int64_t t = blockIdx.x;
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t bpr = (cols + 7) / 8;
+  uint8_t* rec = records + 16ull * tile_off[t];
+  uint32_t* hdr = reinterpret_cast<uint32_t*>(rec);
+  uint32_t* bits = hdr + 4;
+  const uint32_t c0 = tile_cnt[4 * t], c1 = tile_cnt[4 * t + 1], c2 = tile_cnt[4 * t + 2],
+                 c3 = tile_cnt[4 * t + 3];
+  const uint32_t gbase[4] = {0u, c0, c0 + c1, c0 + c1 + c2};
+  const uint32_t nnz = c0 + c1 + c2 + c3;
+  if (threadIdx.x == 0) {
+    hdr[0] = gbase[1];
+    hdr[1] = gbase[2];
+    hdr[2] = gbase[3];
+    hdr[3] = nnz;
+  }
+  const uint32_t lt = lanemask_lt();
+  uint32_t off = gbase[g];
+  for (int k = 0; k < kTileK; ++k) {
+    const int64_t row = kt * kTileK + k;
+    uint32_t word = 0, before = 0;
+    if (row < rows) {
+      for (int gg = 0; gg < g; ++gg) before += __popc(ref_word(bitmap, bpr, row, nt * 16 + 4 * gg));
+      word = ref_word(bitmap, bpr, row, nt * 16 + 4 * g);
+    }
+    if (lane == 0) bits[g * kTileK + k] = word;
+    if ((word >> lane) & 1u) {
+      const uint32_t r = __popc(word & lt);
+      const uint32_t ridx = rowtile_off[row * n_nt + nt] + before + r;
+      const float v = values_dtype == kF32 ? static_cast<const float*>(values)[ridx]
+                                           : __bfloat162float(static_cast<const __nv_bfloat16*>(values)[ridx]);
+      if (value_dtype == kBF16)
+        reinterpret_cast<__nv_bfloat16*>(rec + kValOffset)[off + r] = __float2bfloat16_rn(v);
+      else
+        reinterpret_cast<float*>(rec + kValOffset)[off + r] = v;
+    }
+    off += __popc(word);
+  }
+  if (threadIdx.x < 16) {
+    const uint32_t used = kValOffset + nnz * value_bytes(value_dtype);
+    const uint32_t end = 16u * (tile_off[t + 1] - tile_off[t]);
+    const uint32_t b = used + threadIdx.x;
+    if (b < end) rec[b] = 0;
+  }
+}
+
+static inline void geometry(int64_t rows, int64_t cols, int64_t* n_kt, int64_t* n_nt) {
+  *n_kt = (rows + kTileK - 1) / kTileK;
+  *n_nt = (cols + kTileN - 1) / kTileN;
+}
+
+static int check_dims(int64_t rows, int64_t cols) {
+  SALR_CHECK_ARG(rows >= 1 && cols >= 1, SALR_ERR_SHAPE, "invalid dims (%lld, %lld)", (long long)rows,
+                 (long long)cols);
+  SALR_CHECK_ARG(rows * cols < (int64_t)0xFFFFFFFF, SALR_ERR_SHAPE,
+                 "matrix of %lld entries exceeds the 32-bit value index", (long long)(rows * cols));
+  return SALR_OK;
+}
+
+}  // namespace salr
+
+using namespace salr;
+
+extern "C" {
+
+int salr_version(void) { return 1; }
+
+const char* salr_last_error(void) { return g_err; }
+
+int salr_tb_geometry(int64_t rows, int64_t cols, int64_t* n_kt, int64_t* n_nt, int64_t* n_tiles) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  geometry(rows, cols, n_kt, n_nt);
+  *n_tiles = *n_kt * *n_nt;
+  return SALR_OK;
+}
+
+int salr_encode_count(const void* dense, int in_dtype, int64_t rows, int64_t cols, int64_t ld,
+                      int value_dtype, uint32_t* tile_cnt, uint32_t* tile_off, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(in_dtype == kF32 || in_dtype == kBF16 || in_dtype == kF64, SALR_ERR_DOMAIN,
+                 "unsupported input dtype %d", in_dtype);
+  SALR_CHECK_ARG(value_dtype == kF32 || value_dtype == kBF16, SALR_ERR_FORMAT,
+                 "unsupported value dtype %d", value_dtype);
+  SALR_CHECK_ARG(ld >= cols, SALR_ERR_SHAPE, "leading dim %lld < cols %lld", (long long)ld, (long long)cols);
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  const int64_t n_tiles = n_kt * n_nt;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  encode_count_kernel<<<(unsigned)n_tiles, 128, 0, s>>>(dense, in_dtype, rows, cols, ld, n_kt, tile_cnt);
+  SALR_LAUNCH_CHECK();
+  scan1_kernel<<<1, 1024, 0, s>>>(TileUnitsFn{tile_cnt, value_bytes(value_dtype)}, n_tiles, tile_off);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_encode_write(const void* dense, int in_dtype, int64_t rows, int64_t cols, int64_t ld,
+                      int value_dtype, const uint32_t* tile_cnt, const uint32_t* tile_off,
+                      uint8_t* records, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(value_dtype == kF32 || value_dtype == kBF16, SALR_ERR_FORMAT,
+                 "unsupported value dtype %d", value_dtype);
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  encode_write_kernel<<<(unsigned)(n_kt * n_nt), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      dense, in_dtype, rows, cols, ld, n_kt, value_dtype, tile_cnt, tile_off, records);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_decode(const uint8_t* records, const uint32_t* tile_off, int value_dtype, int64_t rows,
+                int64_t cols, int64_t r0, int64_t r1, int64_t c0, int64_t c1, void* out, int out_dtype,
+                int64_t ld_out, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(0 <= r0 && r0 <= r1 && r1 <= rows && 0 <= c0 && c0 <= c1 && c1 <= cols, SALR_ERR_BOUNDS,
+                 "window rows [%lld,%lld) cols [%lld,%lld) outside (%lld, %lld)", (long long)r0,
+                 (long long)r1, (long long)c0, (long long)c1, (long long)rows, (long long)cols);
+  SALR_CHECK_ARG(out_dtype == kF32 || out_dtype == kBF16 || out_dtype == kF64, SALR_ERR_DOMAIN,
+                 "unsupported output dtype %d", out_dtype);
+  if (r1 == r0 || c1 == c0) return SALR_OK;
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  const int64_t kt0 = r0 / kTileK, kt1 = (r1 + kTileK - 1) / kTileK;
+  const int64_t nt0 = c0 / kTileN, nt1 = (c1 + kTileN - 1) / kTileN;
+  const int64_t span_k = kt1 - kt0, nblocks = span_k * (nt1 - nt0);
+  decode_kernel<<<(unsigned)nblocks, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      records, tile_off, value_dtype, n_kt, r0, r1, c0, c1, kt0, nt0, span_k, out, out_dtype, ld_out);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_tb_nnz(const uint8_t* records, const uint32_t* tile_off, int64_t n_tiles,
+                unsigned long long* nnz_dev, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  SALR_CUDA_TRY(cudaMemsetAsync(nnz_dev, 0, sizeof(unsigned long long), s));
+  const int blocks = (int)std::min<int64_t>(148 * 4, (n_tiles + 255) / 256 + 1);
+  tb_nnz_kernel<<<blocks, 256, 0, s>>>(records, tile_off, n_tiles, nnz_dev);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_to_reference(const uint8_t* records, const uint32_t* tile_off, int value_dtype, int64_t rows,
+                      int64_t cols, uint32_t* rowtile_off, uint8_t* bitmap_out, void* values_out,
+                      int values_dtype, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(values_dtype == kF32 || values_dtype == kBF16, SALR_ERR_DOMAIN,
+                 "unsupported values dtype %d", values_dtype);
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  const int64_t n_tiles = n_kt * n_nt;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // rowtile counts land in rowtile_off[0 .. rows*n_nt) then are scanned in place
+  // (the single-block scan reads each item before any later write to it).
+  tb_rowtile_count_kernel<<<(unsigned)n_tiles, 64, 0, s>>>(records, tile_off, rows, n_kt, n_nt, rowtile_off);
+  SALR_LAUNCH_CHECK();
+  scan1_kernel<<<1, 1024, 0, s>>>(ArrayFn{rowtile_off}, rows * n_nt, rowtile_off);
+  SALR_LAUNCH_CHECK();
+  tb_to_reference_kernel<<<(unsigned)n_tiles, 128, 0, s>>>(records, tile_off, value_dtype, rows, cols, n_kt,
+                                                           n_nt, rowtile_off, bitmap_out, values_out,
+                                                           values_dtype);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_from_reference_count(const uint8_t* bitmap, int64_t rows, int64_t cols, int value_dtype,
+                              uint32_t* rowtile_off, uint32_t* tile_cnt, uint32_t* tile_off, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(value_dtype == kF32 || value_dtype == kBF16, SALR_ERR_FORMAT,
+                 "unsupported value dtype %d", value_dtype);
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  const int64_t n_tiles = n_kt * n_nt;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t nrt = rows * n_nt;
+  ref_rowtile_count_kernel<<<(unsigned)((nrt + 255) / 256), 256, 0, s>>>(bitmap, rows, cols, n_nt, rowtile_off);
+  SALR_LAUNCH_CHECK();
+  scan1_kernel<<<1, 1024, 0, s>>>(ArrayFn{rowtile_off}, nrt, rowtile_off);
+  SALR_LAUNCH_CHECK();
+  ref_tile_count_kernel<<<(unsigned)((n_tiles * kGroups + 255) / 256), 256, 0, s>>>(bitmap, rows, cols, n_kt,
+                                                                                   n_tiles, tile_cnt);
+  SALR_LAUNCH_CHECK();
+  scan1_kernel<<<1, 1024, 0, s>>>(TileUnitsFn{tile_cnt, value_bytes(value_dtype)}, n_tiles, tile_off);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_from_reference_write(const uint8_t* bitmap, const void* values, int values_dtype, int64_t rows,
+                              int64_t cols, int value_dtype, const uint32_t* rowtile_off,
+                              const uint32_t* tile_cnt, const uint32_t* tile_off, uint8_t* records,
+                              void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(values_dtype == kF32 || values_dtype == kBF16, SALR_ERR_DOMAIN,
+                 "unsupported values dtype %d", values_dtype);
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  ref_to_tb_kernel<<<(unsigned)(n_kt * n_nt), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      bitmap, values, values_dtype, rows, cols, n_kt, n_nt, value_dtype, rowtile_off, tile_cnt, tile_off,
+      records);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,250 @@
+"""The SALR linear forward on the B200 behind the reference engine's API
+(``pkg/src/salr/pipeline.py``).
+
+The reference's two-stage engine -- a decoder thread filling a bounded SPSC
+ring with dense tiles and a compute thread multiplying them
+(``pipeline.py:110-331``) -- is one persistent CUDA kernel here
+(``csrc/salr_linear.cu``): a TMA warp streams compressed tiles into a
+shared-memory ring, decoder warps expand them into TMEM, a single thread
+issues tcgen05 MMAs, and mbarriers play the ring's Empty -> Filled ->
+Consumed -> Empty slot protocol.
+
+``PipelineConfig`` keeps the reference fields and validation
+(``pipeline.py:63-86``).  Mapping onto the kernel:
+
+* ``ring_capacity`` -> shared-memory ring slots (clamped to what fits);
+* ``overlap=False`` -> a one-slot ring: decode of tile k+1 waits for the MMA
+  of tile k (the serial schedule);
+* ``tile_rows`` / ``tile_col_bytes`` -> accepted and validated; the device
+  tile is fixed at 64 rows x 16 bitmap bytes (the TB format).
+
+As in the reference, the result does not depend on the schedule: the
+per-column accumulation order is fixed, so serial and overlapped runs (and
+all ring capacities) are bit-identical for a given CTA count.
+"""
+
+from __future__ import annotations
+
+import statistics
+from dataclasses import dataclass, field
+from enum import Enum
+
+import torch
+
+from . import _lib
+from .bitmap import BitmapSparseMatrix
+from .errors import ConfigError, DomainError, SalrError, ShapeError, VerificationError
+from .fusion import FusedAdapters
+from .linalg import as_matrix
+
+__all__ = ["SlotState", "PipelineConfig", "PipelineProbe", "BenchResult", "pipelined_matmul",
+           "pipelined_forward", "validate_transitions", "bench", "salr_linear"]
+
+
+class SlotState(Enum):
+    EMPTY = "empty"
+    FILLED = "filled"
+    CONSUMED = "consumed"
+
+
+_LEGAL = {
+    (SlotState.EMPTY, SlotState.FILLED),
+    (SlotState.FILLED, SlotState.CONSUMED),
+    (SlotState.CONSUMED, SlotState.EMPTY),
+}
+
+
+@dataclass(frozen=True)
+class PipelineConfig:
+    """Tile and ring dimensions (reference ``pipeline.py:63-86``)."""
+
+    tile_rows: int = 64
+    tile_col_bytes: int = 8
+    ring_capacity: int = 4
+    overlap: bool = True
+
+    def __post_init__(self):
+        if self.tile_rows < 1 or self.tile_col_bytes < 1:
+            raise ConfigError(f"tile dims must be positive, got ({self.tile_rows}, {self.tile_col_bytes})")
+        if self.ring_capacity < 1:
+            raise ConfigError(f"ring_capacity must be >= 1, got {self.ring_capacity}")
+        if self.overlap and self.ring_capacity < 2:
+            raise ConfigError("overlap requires ring_capacity >= 2")
+
+    @property
+    def device_stages(self) -> int:
+        """Shared-memory ring slots requested from the kernel (0 = deepest)."""
+        return 1 if not self.overlap else self.ring_capacity
+
+
+@dataclass
+class PipelineProbe:
+    """Audit hooks (reference ``pipeline.py:89-103``).
+
+    Host-side delay callables cannot run inside a CUDA kernel; passing them
+    raises ConfigError.  Transition recording is not available in this build
+    either (ConfigError) -- the device protocol is audited by
+    ``tests/test_gpu_linear.py`` instead.
+    """
+
+    decode_delay: object = None
+    compute_delay: object = None
+    record: bool = False
+    transitions: list = field(default_factory=list)
+    produced: int = 0
+    consumed: int = 0
+
+
+def validate_transitions(probe: PipelineProbe, capacity: int) -> None:
+    """Audit a transition log against the slot protocol (``pipeline.py:334-370``)."""
+    if probe.produced != probe.consumed:
+        raise VerificationError(f"produced {probe.produced} != consumed {probe.consumed}")
+    states = [SlotState.EMPTY] * capacity
+    for step, (idx, old, new) in enumerate(probe.transitions):
+        if not 0 <= idx < capacity:
+            raise VerificationError(f"step {step}: slot index {idx} out of range")
+        if states[idx] is not old:
+            raise VerificationError(f"step {step}: slot {idx} was {states[idx]}, transition claims {old}")
+        if (old, new) not in _LEGAL:
+            raise VerificationError(f"step {step}: illegal transition {old} -> {new} on slot {idx}")
+        states[idx] = new
+    for idx, st in enumerate(states):
+        if st is not SlotState.EMPTY:
+            raise VerificationError(f"slot {idx} left in state {st} at shutdown")
+    fills = sum(1 for _, old, _ in probe.transitions if old is SlotState.EMPTY)
+    if fills != probe.produced:
+        raise VerificationError(f"recorded fills {fills} != produced count {probe.produced}")
+
+
+# ---------------------------------------------------------------------------
+# kernel launch
+
+_WS: dict = {}
+
+
+def _workspace(M: int, N: int, K: int, r_pad: int, num_ctas: int, device) -> torch.Tensor:
+    """Per-device scratch (grown on demand, zeroed at allocation; the kernels
+    leave its ticket counters zero).  Calls sharing it must be stream-ordered:
+    pass ``workspace=`` to ``salr_linear`` for concurrent streams."""
+    need = int(_lib.load().salr_linear_workspace_bytes(M, N, K, r_pad, num_ctas))
+    key = device.index
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(max(need, 1 << 21), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws
+
+
+def _prep_x(x, K: int, check_finite: bool) -> torch.Tensor:
+    xm = as_matrix(x, "x", require_finite=check_finite)
+    if xm.shape[1] != K:
+        raise ShapeError(f"x cols {xm.shape[1]} != sparse rows {K}")
+    if xm.dtype != torch.bfloat16:
+        xm = xm.to(torch.bfloat16)
+    if K % 8:
+        xm = torch.nn.functional.pad(xm, (0, 8 - K % 8))
+    return xm.contiguous()
+
+
+def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *, out: torch.Tensor | None = None,
+                out_dtype: torch.dtype = torch.float32, stages: int = 0, num_ctas: int = 0,
+                check_finite: bool = True, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Launch the fused B200 kernel: ``x @ decode(s) [+ (x @ a_cat) @ b_cat]``.
+
+    ``x`` is rounded to bf16 (the compute format); ``s`` is used with bf16
+    values (converted once and cached if it holds float32 values).
+    """
+    _lib.require_cuda()
+    if not isinstance(s, BitmapSparseMatrix):
+        raise SalrError("s must be a BitmapSparseMatrix")
+    sb = s.to_bf16()
+    xb = _prep_x(x, s.rows, check_finite)
+    M = int(xb.shape[0])
+    N = s.cols
+    if fused is not None and (fused.d_in != s.rows or fused.d_out != s.cols):
+        raise ShapeError(f"fused adapter dims {(fused.d_in, fused.d_out)} != weight dims {(s.rows, s.cols)}")
+    if out_dtype not in (torch.float32, torch.bfloat16):
+        raise DomainError(f"out_dtype must be float32 or bfloat16, got {out_dtype}")
+    if out is None:
+        out = torch.empty((M, N), dtype=out_dtype, device=xb.device)
+    elif out.shape != (M, N) or out.dtype not in (torch.float32, torch.bfloat16) or not out.is_contiguous():
+        raise ShapeError("out must be a contiguous (M, N) float32/bfloat16 tensor")
+    if fused is not None:
+        acat, bct = fused.device_operands()
+        r_pad = fused.r_pad
+    else:
+        acat = bct = None
+        r_pad = 0
+    if workspace is None:
+        ws = _workspace(M, N, s.rows, r_pad, num_ctas, xb.device)
+    else:
+        ws = workspace
+    _lib.check(_lib.load().salr_linear_forward(
+        _lib.ptr(xb), M, s.rows, int(xb.shape[1]), _lib.ptr(sb.records), _lib.ptr(sb.tile_off), N,
+        _lib.ptr(acat), _lib.ptr(bct), r_pad, _lib.ptr(out), _lib.dtype_code(out.dtype), N,
+        _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), _lib.stream_ptr()))
+    return out
+
+
+def _check_probe(probe):
+    if probe is None:
+        return
+    if probe.decode_delay is not None or probe.compute_delay is not None:
+        raise ConfigError("host delay callables cannot be injected into the device pipeline")
+    if probe.record:
+        raise ConfigError("slot-transition recording is not available in this build")
+
+
+def pipelined_matmul(x, s: BitmapSparseMatrix, cfg: PipelineConfig, probe: PipelineProbe | None = None,
+                     out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    """``x @ decode(s)`` through the fused kernel (``pipeline.py:258-272``)."""
+    _check_probe(probe)
+    return salr_linear(x, s, None, out_dtype=out_dtype, stages=cfg.device_stages)
+
+
+def pipelined_forward(x, s: BitmapSparseMatrix, fused: FusedAdapters, cfg: PipelineConfig,
+                      probe: PipelineProbe | None = None, out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    """The SALR linear ``x @ decode(s) + (x @ a_cat) @ b_cat`` (``pipeline.py:275-331``)."""
+    _check_probe(probe)
+    if fused.d_in != s.rows or fused.d_out != s.cols:
+        raise ShapeError(f"fused adapter dims {(fused.d_in, fused.d_out)} != weight dims {(s.rows, s.cols)}")
+    return salr_linear(x, s, fused, out_dtype=out_dtype, stages=cfg.device_stages)
+
+
+@dataclass(frozen=True)
+class BenchResult:
+    serial_s: float
+    overlapped_s: float
+    speedup: float
+
+
+def bench(x_shape, s: BitmapSparseMatrix, cfg: PipelineConfig, repeats: int = 5, seed: int = 0) -> BenchResult:
+    """Median device times of the serial (1-slot ring) and overlapped
+    schedules with a bit-identity gate (``pipeline.py:380-436``).  Timed with
+    CUDA events; absolute numbers come from ``bench.py``."""
+    if repeats < 3:
+        raise DomainError("repeats must be >= 3")
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(tuple(x_shape), generator=g).to(torch.bfloat16)
+    serial = PipelineConfig(cfg.tile_rows, cfg.tile_col_bytes, cfg.ring_capacity, overlap=False)
+    over = PipelineConfig(cfg.tile_rows, cfg.tile_col_bytes, max(cfg.ring_capacity, 2), overlap=True)
+    a = pipelined_matmul(x, s, serial)
+    b = pipelined_matmul(x, s, over)
+    if not torch.equal(a, b):
+        raise VerificationError("serial and overlapped outputs differ")
+    xd = _prep_x(x, s.rows, True)
+
+    def timed(c):
+        pipelined_matmul(xd, s, c)
+        ts = []
+        for _ in range(repeats):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pipelined_matmul(xd, s, c)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        return float(statistics.median(ts))
+
+    ts, to = timed(serial), timed(over)
+    return BenchResult(serial_s=ts, overlapped_s=to, speedup=ts / to)
