@@ -46,9 +46,9 @@ struct LinearParams {
   void* y;
   float* partials;              // [2 * gridDim.x][BM][128] fp32 split-K partial tiles
   uint32_t* tickets;            // n_mc * n_nt, zero on entry and exit
-  int64_t M, N, ldy;
-  int64_t n_kt, n_nt, n_mc;
-  int64_t units;                // n_mc * n_nt * n_kt
+  int M, N, ldy;                // 32-bit indexing: host checks M * max(N, ldy) < 2^31
+  int n_kt, n_nt, n_mc;
+  int units;                    // n_mc * n_nt * n_kt
   int r_pad;                    // 0, 64 or 128
   int y_dtype;
   int stages;                   // ring slots in use, 1 (serial) .. stages_for(BM)
@@ -77,8 +77,8 @@ __host__ __device__ inline SmemPlan smem_plan(int bm, int stages, int r_pad) {
 }
 
 // CTA that owns work unit u under the even contiguous split of `units` over `ctas`.
-__device__ __forceinline__ int64_t cta_of(int64_t u, int64_t units, int64_t ctas) {
-  return ((u + 1) * ctas + units - 1) / units - 1;
+__device__ __forceinline__ int cta_of(int u, int units, int ctas) {
+  return (int)((((int64_t)u + 1) * ctas + units - 1) / units - 1);
 }
 
 template <int BM, int NDEC>
@@ -89,10 +89,13 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
   constexpr int RP = kTileK / NPART;         // rows (K) per decoder warp
   constexpr int ACOLS = RP / 2;              // TMEM columns written per decoder warp
   constexpr uint32_t IDESC = idesc_bf16_f32(128, BM);
-  static_assert(NDEC % 4 == 0 && (ACOLS == 16 || ACOLS == 32), "decoder split");
+  static_assert(NDEC % 4 == 0 && (ACOLS == 8 || ACOLS == 16 || ACOLS == 32), "decoder split");
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 128B-swizzled TMA/UMMA tiles need 1024-byte alignment; pad by an offset
+  // (not a pointer round-trip) so the compiler keeps the shared address space
+  // and emits 32-bit LDS.
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const SmemPlan plan = smem_plan(BM, STAGES, p.r_pad);
   uint8_t* xbuf = smem + plan.x_off;
   uint8_t* ubuf = smem + plan.u_off;
@@ -110,9 +113,9 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
   const uint32_t lane = threadIdx.x & 31;
 
   // ---- per-CTA work range
-  const int64_t G = gridDim.x;
-  const int64_t u_begin = (int64_t)blockIdx.x * p.units / G;
-  const int64_t u_end = ((int64_t)blockIdx.x + 1) * p.units / G;
+  const int G = gridDim.x;
+  const int u_begin = (int)((int64_t)blockIdx.x * p.units / G);
+  const int u_end = (int)(((int64_t)blockIdx.x + 1) * p.units / G);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&xmap);
@@ -135,15 +138,15 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
   if (warp == 0) {
     // ================= TMA producer
     if (lane == 0) {
-      int64_t it = 0;
-      for (int64_t u = u_begin; u < u_end; ++u, ++it) {
+      int it = 0;
+      for (int u = u_begin; u < u_end; ++u, ++it) {
         const int s = (int)(it % p.stages);
         const uint32_t ph = (uint32_t)((it / p.stages) & 1);
         mbar_wait(&empty[s], ph ^ 1);
-        const int64_t kt = u % p.n_kt;
-        const int64_t nt = (u / p.n_kt) % p.n_nt;
-        const int64_t mc = u / (p.n_kt * p.n_nt);
-        const int64_t t = nt * p.n_kt + kt;
+        const int kt = u % p.n_kt;
+        const int nt = (u / p.n_kt) % p.n_nt;
+        const int mc = u / (p.n_kt * p.n_nt);
+        const int t = nt * p.n_kt + kt;
         const uint32_t o0 = p.tile_off[t], o1 = p.tile_off[t + 1];
         const uint32_t bytes = (o1 - o0) * 16u;
         mbar_arrive_expect_tx(&full[s], bytes + BM * 128);
@@ -154,16 +157,16 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
   } else if (warp == 1) {
     // ================= MMA issuer (one thread)
     if (lane == 0) {
-      int64_t it = 0, seg = 0;
+      int it = 0, seg = 0;
       uint32_t ad_phase = 0;
-      int64_t u = u_begin;
+      int u = u_begin;
       while (u < u_end) {
-        const int64_t tile_base = u - u % p.n_kt;
-        const int64_t seg_end = min(u_end, tile_base + p.n_kt);
+        const int tile_base = u - u % p.n_kt;
+        const int seg_end = min(u_end, tile_base + p.n_kt);
         const bool first_k = (u == tile_base);
         mbar_wait(acc_empty, (uint32_t)(seg & 1) ^ 1u);
         tc_fence_after();
-        for (int64_t v = u; v < seg_end; ++v, ++it) {
+        for (int v = u; v < seg_end; ++v, ++it) {
           const int s = (int)(it % p.stages);
           const uint32_t ph = (uint32_t)((it / p.stages) & 1);
           mbar_wait(&full[s], ph);
@@ -201,48 +204,54 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
     const int q = warp & 3;            // TMEM lane quarter == 32-column group
     const int part = dw >> 2;          // which RP-row slice of the tile
     const uint32_t lt = lanemask_lt();
+    const uint32_t lanebit = 1u << lane;
     const uint32_t lane_tm = (uint32_t)(32 * q) << 16;
-    int64_t it = 0, seg = 0;
+    int it = 0, seg = 0;
     bool pdl_done = false;
-    int64_t u = u_begin;
+    int u = u_begin;
     while (u < u_end) {
-      const int64_t tile_base = u - u % p.n_kt;
-      const int64_t seg_end = min(u_end, tile_base + p.n_kt);
+      const int tile_base = u - u % p.n_kt;
+      const int seg_end = min(u_end, tile_base + p.n_kt);
       const bool first_k = (u == tile_base);
       const bool full_cover = first_k && (seg_end == tile_base + p.n_kt);
-      const int64_t nt = (u / p.n_kt) % p.n_nt;
-      const int64_t mc = u / (p.n_kt * p.n_nt);
+      const int nt = (u / p.n_kt) % p.n_nt;
+      const int mc = u / (p.n_kt * p.n_nt);
 
-      for (int64_t v = u; v < seg_end; ++v, ++it) {
+      for (int v = u; v < seg_end; ++v, ++it) {
         const int s = (int)(it % p.stages);
         const uint32_t ph = (uint32_t)((it / p.stages) & 1);
         mbar_wait(&full[s], ph);
-        const uint8_t* rec = recbuf + (size_t)s * kRecSlot;
+        const uint8_t* rec = recbuf + s * kRecSlot;
         const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec);
-        const uint32_t* bits = hdr + 4 + q * kTileK + part * RP;
+        const uint32_t* gbits = hdr + 4 + q * kTileK;         // this group's 64 row words
         const uint16_t* vals = reinterpret_cast<const uint16_t*>(rec + kValOffset);
+        // this warp's RP row words (broadcast loads, all issued up front)
+        uint32_t w[RP];
+#pragma unroll
+        for (int i = 0; i < RP; i += 4) {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(gbits + part * RP + i);
+          w[i] = q4.x; w[i + 1] = q4.y; w[i + 2] = q4.z; w[i + 3] = q4.w;
+        }
         uint32_t off = q == 0 ? 0u : hdr[q - 1];
-        if (part > 0) {
-          // values of this group in the rows before this slice
-          const uint32_t* b0 = hdr + 4 + q * kTileK;
-          uint32_t c = 0;
-          for (int k = (int)lane; k < part * RP; k += 32) c += __popc(b0[k]);
+        if (part > 0) {  // values of this group in the rows before this slice
+          uint32_t c = 0u;
+          for (int k = (int)lane; k < part * RP; k += 32) c += __popc(gbits[k]);
           off += __reduce_add_sync(0xffffffffu, c);
         }
         uint32_t packed[ACOLS];
+        const uint16_t* vp = vals + off;  // first value of the current row
 #pragma unroll
         for (int k2 = 0; k2 < ACOLS; ++k2) {
-          const uint2 w = *reinterpret_cast<const uint2*>(bits + 2 * k2);
-          uint32_t v0 = 0, v1 = 0;
-          if ((w.x >> lane) & 1u) v0 = vals[off + __popc(w.x & lt)];
-          off += __popc(w.x);
-          if ((w.y >> lane) & 1u) v1 = vals[off + __popc(w.y & lt)];
-          off += __popc(w.y);
-          packed[k2] = v0 | (v1 << 16);
+          const uint32_t w0 = w[2 * k2], w1 = w[2 * k2 + 1];
+          const uint16_t* vp1 = vp + __popc(w0);
+          uint32_t v0 = 0u, v1 = 0u;
+          if (w0 & lanebit) v0 = vp[__popc(w0 & lt)];
+          if (w1 & lanebit) v1 = vp1[__popc(w1 & lt)];
+          vp = vp1 + __popc(w1);
+          packed[k2] = __byte_perm(v0, v1, 0x5410);
         }
         const uint32_t taddr = tmem + lane_tm + kAStageCol + 32 * s + ACOLS * part;
-#pragma unroll
-        for (int c = 0; c < ACOLS; c += 16) SALR_TMEM_ST_X16(taddr + c, (packed + c));
+        tmem_st_cols<ACOLS>(taddr, packed);
         tc_wait_st();
         tc_fence_before();
         __syncwarp();
@@ -257,19 +266,19 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
         const int ra = p.r_pad / 64;
         // B_cat^T rows -> TMEM adapter A operand (this warp: lane quarter q, column slice `part`)
         {
-          const int64_t n = nt * kTileN + 32 * q + lane;
+          const int n = nt * kTileN + 32 * q + lane;
           const uint32_t* src = reinterpret_cast<const uint32_t*>(p.bcat_t + (size_t)n * p.r_pad);
           const int cols = p.r_pad / 2;                  // u32 columns of this row
           const int per = cols / NPART;
           const uint32_t ad_tm = tmem + lane_tm + kAStageCol + 32 * STAGES + per * part;
-          for (int c = 0; c < per; c += 16) {
-            uint32_t r[16];
+          for (int c = 0; c < per; c += 8) {
+            uint32_t r[8];
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
+            for (int i = 0; i < 8; i += 4) {
               const uint4 q4 = __ldg(reinterpret_cast<const uint4*>(src + per * part + c + i));
               r[i] = q4.x; r[i + 1] = q4.y; r[i + 2] = q4.z; r[i + 3] = q4.w;
             }
-            SALR_TMEM_ST_X16(ad_tm + c, r);
+            tmem_st_cols<8>(ad_tm + c, r);
           }
         }
         // U (fp32) -> bf16 hi/lo, K-major 128B-swizzled B operand tiles in smem
@@ -278,9 +287,9 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
           for (int i = dw * 32 + (int)lane; i < pairs; i += NDEC * 32) {
             const int m = i / (p.r_pad / 2);
             const int r = 2 * (i % (p.r_pad / 2));
-            const int64_t gm = mc * BM + m;
+            const int gm = mc * BM + m;
             float2 uv = make_float2(0.f, 0.f);
-            if (gm < p.M) uv = *reinterpret_cast<const float2*>(p.u + gm * p.r_pad + r);
+            if (gm < p.M) uv = *reinterpret_cast<const float2*>(p.u + (size_t)gm * p.r_pad + r);
             const __nv_bfloat16 h0 = __float2bfloat16_rn(uv.x), h1 = __float2bfloat16_rn(uv.y);
             const __nv_bfloat16 l0 = __float2bfloat16_rn(uv.x - __bfloat162float(h0));
             const __nv_bfloat16 l1 = __float2bfloat16_rn(uv.y - __bfloat162float(h1));
@@ -307,7 +316,7 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
       {
         constexpr int CPW = BM / NPART;   // columns (tokens) per warp
         const int nl = 32 * q + (int)lane;
-        const int64_t n = nt * kTileN + nl;
+        const int n = nt * kTileN + nl;
         const bool n_ok = n < p.N;
         for (int c0 = 0; c0 < CPW; c0 += 16) {
           uint32_t r[16];
@@ -320,10 +329,10 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
             if (i >= lim) break;
             const float val = __uint_as_float(r[i]);
             if (full_cover) {
-              const int64_t m = mc * BM + col + i;
+              const int m = mc * BM + col + i;
               if (!n_ok || m >= p.M) continue;
-              if (p.y_dtype == kF32) static_cast<float*>(p.y)[m * p.ldy + n] = val;
-              else static_cast<__nv_bfloat16*>(p.y)[m * p.ldy + n] = __float2bfloat16_rn(val);
+              if (p.y_dtype == kF32) static_cast<float*>(p.y)[(size_t)m * p.ldy + n] = val;
+              else static_cast<__nv_bfloat16*>(p.y)[(size_t)m * p.ldy + n] = __float2bfloat16_rn(val);
             } else {
               __stcg(part_tile + (size_t)(col + i) * kTileN + nl, val);
             }
@@ -339,8 +348,8 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
         // the partial tiles of CTAs c_first..c_last in that fixed order.
         __threadfence();
         named_bar_sync(1, NDEC * 32);
-        const int64_t a = tile_base;
-        const int64_t c_first = cta_of(a, p.units, G), c_last = cta_of(a + p.n_kt - 1, p.units, G);
+        const int a = tile_base;
+        const int c_first = cta_of(a, p.units, G), c_last = cta_of(a + p.n_kt - 1, p.units, G);
         if (dw == 0 && lane == 0) {
           const uint32_t old = atomicAdd(&p.tickets[mc * p.n_nt + nt], 1u);
           *last_flag = (old + 1 == (uint32_t)(c_last - c_first + 1)) ? 1u : 0u;
@@ -350,18 +359,18 @@ __global__ void __launch_bounds__(128 + NDEC * 32, 1)
           __threadfence();
           const int tid = dw * 32 + (int)lane;
           const int nl = tid % kTileN;
-          const int64_t n = nt * kTileN + nl;
+          const int n = nt * kTileN + nl;
           for (int mm = tid / kTileN; mm < BM; mm += NDEC * 32 / kTileN) {
-            const int64_t m = mc * BM + mm;
+            const int m = mc * BM + mm;
             if (m >= p.M || n >= p.N) continue;
             float acc = 0.0f;
-            for (int64_t c = c_first; c <= c_last; ++c) {
-              const int64_t cb = c * p.units / G;  // u_begin of CTA c
+            for (int c = c_first; c <= c_last; ++c) {
+              const int cb = (int)((int64_t)c * p.units / G);  // u_begin of CTA c
               const float* pt = p.partials + ((size_t)c * 2 + (cb >= a ? 0 : 1)) * (size_t)BM * kTileN;
               acc += __ldcg(pt + (size_t)mm * kTileN + nl);
             }
-            if (p.y_dtype == kF32) static_cast<float*>(p.y)[m * p.ldy + n] = acc;
-            else static_cast<__nv_bfloat16*>(p.y)[m * p.ldy + n] = __float2bfloat16_rn(acc);
+            if (p.y_dtype == kF32) static_cast<float*>(p.y)[(size_t)m * p.ldy + n] = acc;
+            else static_cast<__nv_bfloat16*>(p.y)[(size_t)m * p.ldy + n] = __float2bfloat16_rn(acc);
           }
           if (tid == 0) p.tickets[mc * p.n_nt + nt] = 0u;
         }
@@ -399,10 +408,29 @@ __global__ void __launch_bounds__(256) adapter_u_kernel(const __nv_bfloat16* __r
   float acc0 = 0.f, acc1 = 0.f;
   const int64_t ma = m0 + ty, mb = m0 + ty + 4;
   const bool va = ma < M, vb = mb < M;
-  for (int64_t k = k0; k < k1; ++k) {
-    const float a = __bfloat162float(acat[k * r_pad + r]);
-    if (va) acc0 = fmaf(__bfloat162float(x[ma * ldx + k]), a, acc0);
-    if (vb) acc1 = fmaf(__bfloat162float(x[mb * ldx + k]), a, acc1);
+  const __nv_bfloat16* xa = x + (va ? ma : 0) * ldx;
+  const __nv_bfloat16* xb = x + (vb ? mb : 0) * ldx;
+  const int kn = (int)(k1 - k0);
+  const __nv_bfloat16* ap = acat + k0 * r_pad + r;
+  int k = 0;
+  for (; k + 8 <= kn; k += 8) {  // 24 independent loads in flight per thread
+    float a[8], fa[8], fb[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      a[i] = __bfloat162float(ap[(k + i) * r_pad]);
+      fa[i] = __bfloat162float(xa[k0 + k + i]);
+      fb[i] = __bfloat162float(xb[k0 + k + i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      acc0 = fmaf(fa[i], a[i], acc0);
+      acc1 = fmaf(fb[i], a[i], acc1);
+    }
+  }
+  for (; k < kn; ++k) {
+    const float a = __bfloat162float(ap[k * r_pad]);
+    acc0 = fmaf(__bfloat162float(xa[k0 + k]), a, acc0);
+    acc1 = fmaf(__bfloat162float(xb[k0 + k]), a, acc1);
   }
   float* part = u_part + (size_t)blockIdx.y * M * r_pad;
   if (va) __stcg(part + ma * r_pad + r, acc0);
@@ -454,7 +482,7 @@ static int sm_count() {
 
 template <int BM>
 static int launch_linear(const CUtensorMap& xmap, const LinearParams& p, int ctas, cudaStream_t s, bool pdl) {
-  constexpr int NDEC = 8;
+  constexpr int NDEC = 16;
   auto kern = salr_linear_kernel<BM, NDEC>;
   const SmemPlan plan = smem_plan(BM, stages_for(BM), p.r_pad);
   SALR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.total));
@@ -559,12 +587,15 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   p.tile_off = tile_off;
   p.bcat_t = static_cast<const __nv_bfloat16*>(bcat_t);
   p.y = y;
-  p.M = M;
-  p.N = N;
-  p.ldy = ldy;
-  p.n_kt = (K + kTileK - 1) / kTileK;
-  p.n_nt = (N + kTileN - 1) / kTileN;
-  p.n_mc = (M + bm - 1) / bm;
+  SALR_CHECK_ARG(M * (ldy > N ? ldy : N) < ((int64_t)1 << 31) && M * r_pad < ((int64_t)1 << 31), SALR_ERR_SHAPE,
+                 "M x N = %lld x %lld exceeds the 32-bit output index", (long long)M, (long long)N);
+  p.M = (int)M;
+  p.N = (int)N;
+  p.ldy = (int)ldy;
+  p.n_kt = (int)((K + kTileK - 1) / kTileK);
+  p.n_nt = (int)((N + kTileN - 1) / kTileN);
+  p.n_mc = (int)((M + bm - 1) / bm);
+  SALR_CHECK_ARG((int64_t)p.n_mc * p.n_nt * p.n_kt < ((int64_t)1 << 31), SALR_ERR_SHAPE, "too many work units");
   p.units = p.n_mc * p.n_nt * p.n_kt;
   p.r_pad = (int)r_pad;
   p.y_dtype = y_dtype;
@@ -599,6 +630,7 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   }
   int64_t ctas = num_ctas > 0 ? num_ctas : sm_count();
   if (ctas > p.units) ctas = p.units;
+  SALR_CHECK_ARG(ctas <= 65535, SALR_ERR_CONFIG, "num_ctas too large");
   int rc;
   switch (bm) {
     case 16: rc = launch_linear<16>(xmap, p, (int)ctas, s, pdl); break;

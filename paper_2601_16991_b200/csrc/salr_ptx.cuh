@@ -142,6 +142,23 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
       : "r"(taddr)                                                                                    \
       : "memory")
 
+#define SALR_TMEM_ST_X8(taddr, r)                                                                   \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),  \
+               "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])  \
+               : "memory")
+
+// Store N (multiple of 8) consecutive 32-bit TMEM columns of this thread's lane.
+template <int N>
+__device__ __forceinline__ void tmem_st_cols(uint32_t taddr, const uint32_t* r) {
+  if constexpr (N % 16 == 0) {
+#pragma unroll
+    for (int c = 0; c < N; c += 16) SALR_TMEM_ST_X16(taddr + c, (r + c));
+  } else {
+#pragma unroll
+    for (int c = 0; c < N; c += 8) SALR_TMEM_ST_X8(taddr + c, (r + c));
+  }
+}
+
 // UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row core-matrix
 // groups 1024 B apart (SBO), sm_100 descriptor version 1.
 __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {

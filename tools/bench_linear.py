@@ -1,0 +1,72 @@
+"""Per-linear device timing of the fused SALR kernel vs cuBLAS dense bf16.
+
+    python tools/bench_linear.py [--tokens 1,8,32] [--shapes q,k,gate,down] [--reps 30]
+
+Weights rotate through --copies distinct encodings (> L2 in aggregate for the
+big shapes) so every launch streams from HBM.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2601_16991_b200 as S
+from paper_2601_16991_b200 import synthetic
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--tokens", default="1,8,32")
+ap.add_argument("--shapes", default="q,k,o,gate,down")
+ap.add_argument("--reps", type=int, default=30)
+ap.add_argument("--copies", type=int, default=6)
+ap.add_argument("--no-adapters", action="store_true")
+ap.add_argument("--ctas", type=int, default=0)
+ap.add_argument("--stages", type=int, default=0)
+ap.add_argument("--cublas", action="store_true")
+a = ap.parse_args()
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6557.4
+g = torch.Generator(device="cuda").manual_seed(0)
+rows = []
+for name in a.shapes.split(","):
+    K, N = synthetic.LLAMA3_8B_LINEARS[name]
+    mats, fus, dense = [], [], []
+    for c in range(a.copies):
+        w = (torch.randn(K, N, generator=g, device="cuda") * 0.02).bfloat16()
+        w = torch.where(w.float().abs() < 0.02 * 0.6744897501960817, torch.zeros_like(w), w)
+        mats.append(S.encode(w, value_dtype="bf16"))
+        f = None if a.no_adapters else S.fuse([
+            S.AdapterPair(torch.randn(K, 16, device="cuda") / 64, torch.randn(16, N, device="cuda") * 0.02, 16),
+            S.AdapterPair(torch.randn(K, 16, device="cuda") / 64, torch.randn(16, N, device="cuda") * 0.02, 16, 2.0)])
+        fus.append(f)
+        if a.cublas and c < 4:
+            dense.append(w)
+        del w
+    for M in [int(t) for t in a.tokens.split(",")]:
+        x = torch.randn(M, K, device="cuda").bfloat16()
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        for i in range(3):
+            S.salr_linear(x, mats[i % a.copies], fus[i % a.copies], out=out, check_finite=False, num_ctas=a.ctas, stages=a.stages)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(a.reps):
+            S.salr_linear(x, mats[i % a.copies], fus[i % a.copies], out=out, check_finite=False, num_ctas=a.ctas, stages=a.stages)
+        e1.record(); e1.synchronize()
+        us = 1e3 * e0.elapsed_time(e1) / a.reps
+        cb = mats[0].compressed_bytes
+        row = {"linear": name, "M": M, "us": round(us, 2), "GBs": round(cb / us / 1e3, 1), "frac": round(cb / us / 1e3 / peak, 3)}
+        if a.cublas:
+            for i in range(3):
+                torch.matmul(x, dense[i % len(dense)])
+            torch.cuda.synchronize()
+            e0.record()
+            for i in range(a.reps):
+                torch.matmul(x, dense[i % len(dense)])
+            e1.record(); e1.synchronize()
+            cus = 1e3 * e0.elapsed_time(e1) / a.reps
+            row["cublas_us"] = round(cus, 2)
+            row["speedup"] = round(cus / us, 3)
+        rows.append(row)
+        print(json.dumps(row), flush=True)
