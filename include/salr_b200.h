@@ -119,6 +119,10 @@ int salr_from_reference_write(const uint8_t* bitmap, const void* values, int val
  *   calls.  Split-K partials are summed in a fixed order: results are
  *   bit-identical from run to run for a given num_ctas. */
 size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pad, int num_ctas);
+/* Instrumentation (tools only): when buf != NULL, subsequent linear launches
+ * write per-CTA %globaltimer stamps of pipeline events into buf[cta][32]
+ * (u64, device memory, >= 32 * 8 * num_ctas bytes).  NULL disables. */
+int salr_debug_set_trace(void* buf);
 int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const uint8_t* records,
                         const uint32_t* tile_off, int64_t N, const void* acat, const void* bcat_t,
                         int64_t r_pad, void* y, int y_dtype, int64_t ldy, void* workspace,

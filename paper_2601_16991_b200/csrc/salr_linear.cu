@@ -1,33 +1,45 @@
 // SALR linear forward on sm_100a:  Y = X @ decode(W) + (X @ A_cat) @ B_cat
 //
-// Reference: pkg/src/salr/pipeline.py:405-461 (pipelined_forward: stage-1
+// Reference: pkg/src/salr/pipeline.py:275-331 (pipelined_forward: stage-1
 // bitmap decode into tiles, stage-2 tile products, adapter delta added once),
 // pkg/src/salr/fusion.py:87-92 (apply_fused: exactly two products).
 //
 // B200 design:
-//   * swap-AB: the tensor core computes Y^T tile = W^T tile (128 output cols,
-//     M_mma = 128) x X^T (N_mma = BM tokens) with the fp32 accumulator in TMEM.
-//   * stage 1 (decode) is a producer warpgroup: decoder thread (warp q, lane
-//     l) owns output column n = 32q + l of the tile == TMEM lane 32q + l and
-//     expands that column's bitmap bits into bf16 pairs along K, written
-//     straight into TMEM with tcgen05.st -- the A operand of tcgen05.mma is
-//     read from TMEM, so decoded tiles never touch shared memory.
-//   * TMA: one warp streams each compressed tile record (1-D bulk copy) and
-//     the matching X tile (2-D tensor map, 128B swizzle) into a ring of
-//     STAGES shared-memory slots (full/empty mbarriers, expect_tx).
-//   * one thread issues tcgen05.mma; tcgen05.commit frees the ring slot and
-//     the TMEM A stage, so decode of tile k+1 overlaps the MMA of tile k (the
-//     GPU form of the reference's SPSC ring, pipeline.py:110-183).
+//   * swap-AB: the tensor core computes a Y^T tile = W^T tile (128 output
+//     columns = M_mma 128) x X^T (N_mma = BM tokens), fp32 accumulator in TMEM.
+//   * warp roles of one persistent CTA per SM (24 warps):
+//       warp 0      TMA producer: each compressed tile record (1-D bulk copy)
+//                   and its X tile (2-D tensor map, 128B swizzle) into a ring
+//                   of shared-memory stages (full/empty mbarriers, expect_tx);
+//                   adapter operands (B_cat^T tile, U hi/lo) per output tile.
+//       warp 1      MMA issuer (one thread), TMEM allocator.
+//       warp 2      row-base warp: per stage, the exclusive prefix of the
+//                   bitmap row popcounts (warp scan) -> smem table of the
+//                   shared-memory byte offset where every (group, row) run of
+//                   compacted values starts.
+//       warps 4-19  decoders, four groups of four warps.  Group t decodes
+//                   tiles it = t (mod 4); warp (t, q) owns output columns
+//                   32q..32q+31 == TMEM lanes 32q..32q+31 and expands all 64
+//                   rows of that column group: value = bits & lanebit ?
+//                   vals[rowbase + popc(bits & lanemask_lt)] : 0, packed as
+//                   bf16 pairs along K and written with tcgen05.st straight
+//                   into the TMEM A operand of the next MMA -- decoded tiles
+//                   never touch shared memory.
+//       warps 20-23 epilogue: TMEM accumulator -> registers -> Y (or an fp32
+//                   split-K partial + fixed-order fixup).
+//   * the ring is the GPU form of the reference's SPSC _Ring
+//     (pipeline.py:110-183): decode of tile k+1 overlaps the MMA of tile k.
 //   * adapters: U = X @ A_cat is produced by a small pre-kernel (PDL
-//     overlapped); the CTA that owns k-tile 0 of an output tile adds
-//     B_cat^T x U^T (hi + lo bf16 split of U) into the SAME TMEM accumulator,
-//     so Y leaves the chip once.
+//     overlapped) as bf16 hi + lo halves; the CTA that owns k-tile 0 of an
+//     output tile adds B_cat^T x [U_hi | U_lo]^T into the SAME TMEM
+//     accumulator (two SMEM-operand MMAs), so Y leaves the chip once.
 //   * stream-K: every CTA owns a contiguous range of (m-chunk, n-tile, k-tile)
 //     work units; a CTA that covers only part of an output tile's K range
-//     stores its fp32 partial tile, and the last CTA to finish that tile sums
+//     stores its fp32 partial tile and the last CTA to finish that tile sums
 //     the partials in a fixed CTA order -- results are bit-identical from run
-//     to run (the reference's schedule-independence, pipeline.py:1-13).
+//     to run (the reference's schedule independence, test_pipeline.py:90-112).
 #include <cstdint>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -41,362 +53,656 @@ namespace salr {
 struct LinearParams {
   const uint8_t* records;
   const uint32_t* tile_off;
-  const __nv_bfloat16* bcat_t;  // (n_nt*128) x r_pad, or nullptr
-  const float* u;               // M x r_pad fp32 (X @ A_cat), or nullptr
   void* y;
-  float* partials;              // [2 * gridDim.x][BM][128] fp32 split-K partial tiles
-  uint32_t* tickets;            // n_mc * n_nt, zero on entry and exit
-  int M, N, ldy;                // 32-bit indexing: host checks M * max(N, ldy) < 2^31
+  float* partials;    // [2 * gridDim.x][BM][128] fp32 split-K partial tiles
+  uint32_t* tickets;  // n_mc * n_nt, zero on entry and exit
+  int M, N, ldy;      // 32-bit indexing: host checks M * max(N, ldy) < 2^31
   int n_kt, n_nt, n_mc;
-  int units;                    // n_mc * n_nt * n_kt
-  int r_pad;                    // 0, 64 or 128
+  int units;          // n_mc * n_nt * n_kt
+  int ra;             // adapter rank blocks of 64 (0 = no adapters)
+  int u_mode;         // 1 = U computed in-kernel (fixed-point atomics), 2 = U hi/lo from the pre-kernel
+  int K;              // d_in (for the in-kernel U slices)
+  const __nv_bfloat16* x;      // X (M x K, ld ldx) for the in-kernel U
+  const __nv_bfloat16* acat;   // A_cat (K x 64*ra) for the in-kernel U
+  int ldx;
+  unsigned long long* u_acc;   // [2][M][64*ra] int64 fixed point (2^kUFrac), parity-buffered
+  uint32_t* ctrl;              // adapter control words (fixed workspace offset)
   int y_dtype;
-  int stages;                   // ring slots in use, 1 (serial) .. stages_for(BM)
+  int stages;         // ring slots in use
+  int dbg;            // timing experiments only: 1 = skip decode, 2 = skip record loads
+  unsigned long long* trace;  // optional per-CTA event timestamps (globaltimer ns), [G][32]
+  // shared-memory carve-up (bytes from the 1024-aligned base)
+  uint32_t x_off, rec_off, base_off, ad_off, bar_off;
 };
 
 constexpr int kRecSlot = kMaxRecordBytesBf16;  // 17424, multiple of 16
-constexpr int kTmemCols = 512;
-constexpr int kAccCol = 0;
-constexpr int kAStageCol = 256;                // A stage s at 256 + 32 s
+// In-kernel U = X @ A_cat: every CTA adds the partial of its K slice into an
+// int64 fixed-point accumulator (2^-kUFrac resolution).  Integer addition is
+// associative, so U is bit-reproducible whatever the CTA order.
+constexpr int kUFrac = 26;
+// ctrl words: [0] epoch (parity selects the U buffer), [1] done counter,
+// [2..3] u_ready[parity], [4..5] used elements of u_acc[parity]
+constexpr int kCtrlEpoch = 0, kCtrlDone = 1, kCtrlReady = 2, kCtrlUsed = 4;
+constexpr int kUAccElems = 256 * 128;  // per parity buffer: M <= 256 rows x r_pad <= 128
+constexpr int kNumDecWarps = 16;
+constexpr int kNumThreads = 800;               // 25 warps
+constexpr int kFirstDecWarp = 4;
+constexpr int kFirstEpiWarp = 20;
+constexpr uint32_t kAdTileBytes = 128 * 128;   // B_cat^T tile: 128 rows x 64 bf16
+constexpr size_t kSmemMax = 232448;            // 227 KB opt-in per block
 
-__host__ __device__ constexpr int stages_for(int bm) { return bm <= 64 ? 6 : (bm <= 128 ? 4 : 3); }
+__host__ __device__ constexpr int nacc_for(int bm) { return bm <= 128 ? 2 : 1; }
+__host__ __device__ constexpr int acc_cols_for(int bm) { return bm < 32 ? 32 : bm; }
 
 struct SmemPlan {
-  uint32_t x_off, u_off, rec_off, bar_off, total;
+  uint32_t x_off, rec_off, base_off, ad_off, bar_off, total;
 };
-__host__ __device__ inline SmemPlan smem_plan(int bm, int stages, int r_pad) {
+// stage-dependent layout; 1024-aligned pieces first (swizzled TMA/UMMA tiles)
+__host__ __device__ inline SmemPlan smem_plan(int bm, int stages, int ra) {
   SmemPlan p;
-  p.x_off = 0;
-  p.u_off = p.x_off + stages * bm * 128;
-  const int ra = r_pad / 64;
-  p.rec_off = p.u_off + 2 * ra * bm * 128;
-  p.bar_off = p.rec_off + stages * kRecSlot;
-  p.bar_off = (p.bar_off + 15) & ~15u;
-  p.total = p.bar_off + 8 * (3 * stages + 3) + 16 + 1024;  // + slack for 1024 alignment
+  p.ad_off = 0;                                            // ra x (Bcat tile + U hi + U lo)
+  const uint32_t ad_bytes = (uint32_t)ra * (kAdTileBytes + 2u * bm * 128u);
+  p.x_off = p.ad_off + ad_bytes;                           // stages x BM x 128 B
+  p.rec_off = p.x_off + (uint32_t)stages * bm * 128u;      // stages x kRecSlot
+  p.base_off = p.rec_off + (uint32_t)stages * kRecSlot;    // stages x 256 u32
+  p.bar_off = p.base_off + (uint32_t)stages * 1024u;
+  p.total = p.bar_off + 8u * (4u * stages + 6u) + 16u + 1024u;  // + tmem slot + alignment slack
   return p;
 }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// per-unit detail for CTA 0 (first 64 units): slot 148*32 + ev*64 + i
+#define SALR_TRACE_UNIT(ev, i)                                                               \
+  do {                                                                                       \
+    if (p.trace && blockIdx.x == 0 && (i) < 64) p.trace[148 * 32 + (ev) * 64 + (i)] = clock64(); \
+  } while (0)
+#define SALR_TRACE(ev) \
+  do {                 \
+    if (p.trace) p.trace[(size_t)blockIdx.x * 32 + (ev)] = globaltimer(); \
+  } while (0)
 
 // CTA that owns work unit u under the even contiguous split of `units` over `ctas`.
 __device__ __forceinline__ int cta_of(int u, int units, int ctas) {
   return (int)((((int64_t)u + 1) * ctas + units - 1) / units - 1);
 }
 
-template <int BM, int NDEC>
-__global__ void __launch_bounds__(128 + NDEC * 32, 1)
-    salr_linear_kernel(const __grid_constant__ CUtensorMap xmap, const LinearParams p) {
-  constexpr int STAGES = stages_for(BM);
-  constexpr int NPART = NDEC / 4;            // decoder warps per TMEM lane quarter
-  constexpr int RP = kTileK / NPART;         // rows (K) per decoder warp
-  constexpr int ACOLS = RP / 2;              // TMEM columns written per decoder warp
+// acq_rel ticket: orders this thread's prior (fenced-by-CTA-barrier) writes
+// before the increment and the reads after it behind it, at GPU scope.
+__device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
+  return old;
+}
+
+// Warp roles (see the file header).  Every mbarrier hand-off costs ~150-300
+// SM cycles of latency on B200 (measured, tools/ubench/ubench_sync.cu), so
+// each serial role is split across warps that work on different units
+// concurrently: two producers (even / odd units), two row-base warps, and
+// kDecGroups decoder groups (group g decodes units it = g mod kDecGroups).
+constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPrep0 = 2, kWarpPrep1 = 3;
+constexpr int kWarpProd1 = 24;
+
+template <int BM, int kDecGroups>
+__global__ void __launch_bounds__(kNumThreads, 1)
+    salr_linear_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
+                       const __grid_constant__ CUtensorMap uhimap, const __grid_constant__ CUtensorMap ulomap,
+                       const LinearParams p) {
+  constexpr int NACC = nacc_for(BM);
+  constexpr int ACOLS = acc_cols_for(BM);
   constexpr uint32_t IDESC = idesc_bf16_f32(128, BM);
-  static_assert(NDEC % 4 == 0 && (ACOLS == 8 || ACOLS == 16 || ACOLS == 32), "decoder split");
+  constexpr int WPG = kNumDecWarps / kDecGroups;  // decoder warps per group
+  constexpr int RPW = 4 * kTileK / WPG;           // rows per decoder warp (all 4 lane quarters per group)
 
   extern __shared__ uint8_t smem_raw[];
   // 128B-swizzled TMA/UMMA tiles need 1024-byte alignment; pad by an offset
-  // (not a pointer round-trip) so the compiler keeps the shared address space
-  // and emits 32-bit LDS.
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const SmemPlan plan = smem_plan(BM, STAGES, p.r_pad);
-  uint8_t* xbuf = smem + plan.x_off;
-  uint8_t* ubuf = smem + plan.u_off;
-  uint8_t* recbuf = smem + plan.rec_off;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + plan.bar_off);
-  uint64_t* empty = full + STAGES;
-  uint64_t* decoded = empty + STAGES;
-  uint64_t* acc_full = decoded + STAGES;
-  uint64_t* acc_empty = acc_full + 1;
-  uint64_t* ad_ready = acc_empty + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ad_ready + 1);
+  // (not a pointer round-trip) so the compiler keeps the shared address space.
+  const uint32_t pad = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  uint8_t* smem = smem_raw + pad;
+  const int S = p.stages;
+  uint8_t* xbuf = smem + p.x_off;
+  uint8_t* recbuf = smem + p.rec_off;
+  uint32_t* basetab = reinterpret_cast<uint32_t*>(smem + p.base_off);
+  uint8_t* adbuf = smem + p.ad_off;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + S;
+  uint64_t* prepd = empty + S;
+  uint64_t* decoded = prepd + S;
+  uint64_t* acc_full = decoded + S;    // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint64_t* ad_full = acc_empty + 2;
+  uint64_t* ad_empty = ad_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ad_empty + 1);
   volatile uint32_t* last_flag = tmem_slot + 1;
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) SALR_TRACE(10);
+  if (threadIdx.x == 0 && p.trace && blockIdx.x == 0) p.trace[148 * 32 + 7 * 64] = clock64();
 
   // ---- per-CTA work range
   const int G = gridDim.x;
   const int u_begin = (int)((int64_t)blockIdx.x * p.units / G);
   const int u_end = (int)(((int64_t)blockIdx.x + 1) * p.units / G);
+  const int tiles_per_mc = p.n_nt * p.n_kt;
 
-  if (warp == 0 && lane == 0) {
-    prefetch_tmap(&xmap);
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-      mbar_init(&decoded[s], NDEC);
+  // ---- producer state (warps kWarpProd0 / kWarpProd1, units of one parity).
+  // Record offsets are fetched 32 units at a time, one chunk ahead, one
+  // coalesced load per lane, so the issue loop never waits on a global load.
+  const int pk = warp == kWarpProd1 ? 1 : 0;
+  uint32_t co0 = 0, co1 = 0, no0 = 0, no1 = 0;
+  int chunk = u_begin;
+  int pv = u_begin + pk;  // next unit to issue (this producer's parity)
+  int ps = pk % S;
+  uint32_t pph = (uint32_t)((pk / S) & 1);
+  auto load_chunk = [&](int c0, uint32_t& o0, uint32_t& o1) {
+    const int v = c0 + (int)lane;
+    o0 = o1 = 0u;
+    if (v < u_end) {
+      const int t = v % tiles_per_mc;
+      o0 = __ldg(p.tile_off + t);
+      o1 = __ldg(p.tile_off + t + 1);
     }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, NDEC);
-    mbar_init(ad_ready, NDEC);
-    fence_barrier_init();
+  };
+  auto issue_one = [&]() {
+    while (pv - chunk >= 32) {
+      chunk += 32;
+      co0 = no0;
+      co1 = no1;
+      load_chunk(chunk + 32, no0, no1);
+    }
+    const uint32_t o0 = __shfl_sync(0xffffffffu, co0, pv - chunk);
+    const uint32_t o1 = __shfl_sync(0xffffffffu, co1, pv - chunk);
+    mbar_wait(&empty[ps], pph ^ 1);
+    if (lane == 0) {
+      const int kt = pv % p.n_kt;
+      const int mc = pv / tiles_per_mc;
+      const uint32_t bytes = (o1 - o0) * 16u;
+      if (p.dbg & 2) {
+        mbar_arrive_expect_tx(&full[ps], BM * 128);
+      } else {
+        mbar_arrive_expect_tx(&full[ps], bytes + BM * 128);
+        bulk_g2s(recbuf + (size_t)ps * kRecSlot, p.records + (size_t)o0 * 16u, bytes, &full[ps]);
+      }
+      tma_2d_g2s(xbuf + (size_t)ps * BM * 128, &xmap, kt * kTileK, mc * BM, &full[ps]);
+      SALR_TRACE_UNIT(0, pv - u_begin);
+    }
+    __syncwarp();
+    ps += 2;
+    while (ps >= S) { ps -= S; pph ^= 1; }
+    pv += 2;
+  };
+
+  if (warp == kWarpProd0 || warp == kWarpProd1) {
+    load_chunk(u_begin, co0, co1);
+    load_chunk(u_begin + 32, no0, no1);
+    if (warp == kWarpProd0 && lane == 0) {
+      prefetch_tmap(&xmap);
+      if (p.ra) {
+        prefetch_tmap(&bmap);
+        prefetch_tmap(&uhimap);
+        prefetch_tmap(&ulomap);
+      }
+      for (int s = 0; s < S; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+        mbar_init(&prepd[s], 1);
+        mbar_init(&decoded[s], WPG);
+      }
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&acc_full[b], 1);
+        mbar_init(&acc_empty[b], 4);
+      }
+      mbar_init(ad_full, 1);
+      mbar_init(ad_empty, 1);
+      fence_barrier_init();
+    }
+    named_bar_sync(2, 64);  // barriers initialised before either producer uses them
+    // Start streaming before the CTA-wide setup barrier: this producer's share
+    // of the first ring's worth of units of the first output tile (never blocks).
+    const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
+    const int pre = min(first_seg_end, u_begin + S);
+    while (pv < pre) issue_one();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kWarpMma) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) SALR_TRACE(0);
+  const uint32_t a_col0 = (uint32_t)((NACC * ACOLS + 31) & ~31);  // first A-stage column
 
-  if (warp == 0) {
-    // ================= TMA producer
-    if (lane == 0) {
-      int it = 0;
-      for (int u = u_begin; u < u_end; ++u, ++it) {
-        const int s = (int)(it % p.stages);
-        const uint32_t ph = (uint32_t)((it / p.stages) & 1);
-        mbar_wait(&empty[s], ph ^ 1);
-        const int kt = u % p.n_kt;
-        const int nt = (u / p.n_kt) % p.n_nt;
-        const int mc = u / (p.n_kt * p.n_nt);
-        const int t = nt * p.n_kt + kt;
-        const uint32_t o0 = p.tile_off[t], o1 = p.tile_off[t + 1];
-        const uint32_t bytes = (o1 - o0) * 16u;
-        mbar_arrive_expect_tx(&full[s], bytes + BM * 128);
-        bulk_g2s(recbuf + (size_t)s * kRecSlot, p.records + (size_t)o0 * 16u, bytes, &full[s]);
-        tma_2d_g2s(xbuf + (size_t)s * BM * 128, &xmap, (int32_t)(kt * kTileK), (int32_t)(mc * BM), &full[s]);
-      }
-    }
-  } else if (warp == 1) {
+  if (warp == kWarpProd0 || warp == kWarpProd1) {
+    // ================= TMA producers
+    if (lane == 0 && pk == 0) SALR_TRACE(1);
+    while (pv < u_end) issue_one();
+    if (lane == 0 && pk == 0) SALR_TRACE(2);
+  } else if (warp == kWarpMma) {
     // ================= MMA issuer (one thread)
     if (lane == 0) {
-      int it = 0, seg = 0;
-      uint32_t ad_phase = 0;
+      int s = 0, seg = 0;
+      uint32_t ph = 0, ad_ph = 0;
       int u = u_begin;
       while (u < u_end) {
         const int tile_base = u - u % p.n_kt;
         const int seg_end = min(u_end, tile_base + p.n_kt);
-        const bool first_k = (u == tile_base);
-        mbar_wait(acc_empty, (uint32_t)(seg & 1) ^ 1u);
+        const int b = NACC == 2 ? (seg & 1) : 0;
+        const uint32_t acc_ph = (uint32_t)((NACC == 2 ? seg >> 1 : seg) & 1);
+        const uint32_t acc = tmem + (uint32_t)(b * ACOLS);
+        mbar_wait(&acc_empty[b], acc_ph ^ 1);
         tc_fence_after();
-        for (int v = u; v < seg_end; ++v, ++it) {
-          const int s = (int)(it % p.stages);
-          const uint32_t ph = (uint32_t)((it / p.stages) & 1);
-          mbar_wait(&full[s], ph);
+        for (int v = u; v < seg_end; ++v) {
           mbar_wait(&decoded[s], ph);
           tc_fence_after();
           const uint64_t bdesc = desc_kmajor_sw128(smem_u32(xbuf + (size_t)s * BM * 128));
-          const uint32_t a_tm = tmem + kAStageCol + 32 * s;
+          const uint32_t a_tm = tmem + a_col0 + 32u * s;
 #pragma unroll
           for (int j = 0; j < kTileK / 16; ++j)
-            mma_ts(tmem + kAccCol, a_tm + 8 * j, bdesc + 2 * j, IDESC, (v != u || j) ? 1u : 0u);
+            mma_ts(acc, a_tm + 8 * j, bdesc + 2 * j, IDESC, (v != u || j) ? 1u : 0u);
           tc_commit(&empty[s]);
+          if (v == u_begin) SALR_TRACE(5);
+          SALR_TRACE_UNIT(5, v - u_begin);
+          if (++s == S) { s = 0; ph ^= 1; }
         }
-        if (first_k && p.r_pad > 0) {
-          mbar_wait(ad_ready, ad_phase);
-          ad_phase ^= 1u;
+        if (u == tile_base && p.ra) {
+          mbar_wait(ad_full, ad_ph);
+          ad_ph ^= 1;
           tc_fence_after();
-          const int ra = p.r_pad / 64;
-          const uint32_t ad_tm = tmem + kAStageCol + 32 * STAGES;
-          for (int half = 0; half < 2; ++half) {
-            for (int a = 0; a < ra; ++a) {
-              const uint64_t ud = desc_kmajor_sw128(smem_u32(ubuf + (size_t)(half * ra + a) * BM * 128));
+          for (int a = 0; a < p.ra; ++a) {
+            uint8_t* blk = adbuf + (size_t)a * (kAdTileBytes + 2u * BM * 128u);
+            const uint64_t adesc = desc_kmajor_sw128(smem_u32(blk));
+            const uint64_t hdesc = desc_kmajor_sw128(smem_u32(blk + kAdTileBytes));
+            const uint64_t ldesc = desc_kmajor_sw128(smem_u32(blk + kAdTileBytes + BM * 128));
 #pragma unroll
-              for (int j = 0; j < 4; ++j) mma_ts(tmem + kAccCol, ad_tm + 32 * a + 8 * j, ud + 2 * j, IDESC, 1u);
-            }
+            for (int j = 0; j < 4; ++j) mma_ss(acc, adesc + 2 * j, hdesc + 2 * j, IDESC, 1u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) mma_ss(acc, adesc + 2 * j, ldesc + 2 * j, IDESC, 1u);
           }
+          tc_commit(ad_empty);
         }
-        tc_commit(acc_full);
+        tc_commit(&acc_full[b]);
+        SALR_TRACE(6);
         ++seg;
         u = seg_end;
       }
     }
-  } else if (warp >= 4) {
-    // ================= decoders (+ adapter staging + epilogue)
-    const int dw = warp - 4;
-    const int q = warp & 3;            // TMEM lane quarter == 32-column group
-    const int part = dw >> 2;          // which RP-row slice of the tile
+  } else if (warp == kWarpPrep0 || warp == kWarpPrep1) {
+    // ================= row bases (two warps, alternate units): exclusive
+    // prefix of the bitmap row popcounts per 32-column group -> smem table of
+    // the shared-memory byte address where each (group, row) value run starts.
+    // lane l handles rows 2l, 2l+1 of all four groups.
+    const int w2 = warp - kWarpPrep0;
+    int s = w2 % S;
+    uint32_t ph = (uint32_t)((w2 / S) & 1);
+    for (int it = u_begin + w2; it < u_end; it += 2) {
+      mbar_wait(&full[s], ph);
+      if (lane == 0) SALR_TRACE_UNIT(1, it - u_begin);
+      const uint8_t* rec = recbuf + (size_t)s * kRecSlot;
+      const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec);
+      const uint32_t* bits = hdr + 4;
+      uint32_t ca[4], cb[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint2 wv = *reinterpret_cast<const uint2*>(bits + g * kTileK + 2 * lane);
+        ca[g] = __popc(wv.x);
+        cb[g] = __popc(wv.y);
+      }
+      // two 16-bit lanes per register: counts per lane <= 64, prefixes <= 4096
+      uint32_t p01 = (ca[0] + cb[0]) | ((ca[1] + cb[1]) << 16);
+      uint32_t p23 = (ca[2] + cb[2]) | ((ca[3] + cb[3]) << 16);
+      const uint32_t own01 = p01, own23 = p23;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t01 = __shfl_up_sync(0xffffffffu, p01, d);
+        const uint32_t t23 = __shfl_up_sync(0xffffffffu, p23, d);
+        if ((int)lane >= d) {
+          p01 += t01;
+          p23 += t23;
+        }
+      }
+      p01 -= own01;
+      p23 -= own23;
+      const uint32_t vbase = smem_u32(rec) + kValOffset;
+      const uint32_t goff[4] = {0u, hdr[0], hdr[1], hdr[2]};
+      const uint32_t ex[4] = {p01 & 0xffffu, p01 >> 16, p23 & 0xffffu, p23 >> 16};
+      uint32_t* tab = basetab + (size_t)s * 256;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint32_t b0 = vbase + 2u * (goff[g] + ex[g]);
+        *reinterpret_cast<uint2*>(tab + g * kTileK + 2 * lane) = make_uint2(b0, b0 + 2u * ca[g]);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&prepd[s]);
+        SALR_TRACE(it == u_begin ? 3 : 12);
+        SALR_TRACE_UNIT(2, it - u_begin);
+      }
+      s += 2;
+      while (s >= S) { s -= S; ph ^= 1; }
+    }
+  } else if (warp >= kFirstDecWarp && warp < kFirstEpiWarp) {
+    // ================= decoders.  Group g = units it = g (mod kDecGroups);
+    // warp (g, part, q) owns TMEM lanes 32q..32q+31 (output columns of group
+    // q) and rows part*RPW .. part*RPW + RPW - 1 of the tile.
+    const int dw = warp - kFirstDecWarp;
+    const int grp = dw / WPG;
+    const int part = (dw % WPG) >> 2;
+    const int q = warp & 3;
     const uint32_t lt = lanemask_lt();
     const uint32_t lanebit = 1u << lane;
     const uint32_t lane_tm = (uint32_t)(32 * q) << 16;
-    int it = 0, seg = 0;
-    bool pdl_done = false;
+    const uint32_t raw_u32 = smem_u32(smem_raw);
+    int s = grp % S;
+    uint32_t ph = (uint32_t)((grp / S) & 1);
+    for (int it = u_begin + grp; it < u_end; it += kDecGroups) {
+      mbar_wait(&full[s], ph);
+      mbar_wait(&prepd[s], ph);
+      const uint32_t* bits =
+          reinterpret_cast<const uint32_t*>(recbuf + (size_t)s * kRecSlot) + 4 + q * kTileK + RPW * part;
+      const uint32_t* tab = basetab + (size_t)s * 256 + q * kTileK + RPW * part;
+      const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(RPW / 2 * part);
+      if (!(p.dbg & 1)) {
+#pragma unroll
+        for (int c = 0; c < RPW / 16; ++c) {  // 16-row chunks -> 8 TMEM columns
+          uint32_t w[16], bs[16];
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const uint4 wv = *reinterpret_cast<const uint4*>(bits + 16 * c + i);
+            const uint4 bv = *reinterpret_cast<const uint4*>(tab + 16 * c + i);
+            w[i] = wv.x; w[i + 1] = wv.y; w[i + 2] = wv.z; w[i + 3] = wv.w;
+            bs[i] = bv.x; bs[i + 1] = bv.y; bs[i + 2] = bv.z; bs[i + 3] = bv.w;
+          }
+          uint32_t packed[8];
+#pragma unroll
+          for (int i = 0; i < 16; i += 2) {
+            uint32_t v0 = 0u, v1 = 0u;
+            if (w[i] & lanebit)
+              v0 = *reinterpret_cast<const uint16_t*>(smem_raw + (bs[i] - raw_u32 + 2u * __popc(w[i] & lt)));
+            if (w[i + 1] & lanebit)
+              v1 = *reinterpret_cast<const uint16_t*>(smem_raw +
+                                                      (bs[i + 1] - raw_u32 + 2u * __popc(w[i + 1] & lt)));
+            packed[i >> 1] = __byte_perm(v0, v1, 0x5410);
+          }
+          SALR_TMEM_ST_X8(taddr + 8u * c, packed);
+        }
+        tc_wait_st();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&decoded[s]);
+        if (dw == 0) SALR_TRACE(it == u_begin ? 4 : 11);
+        if (dw == 0) SALR_TRACE_UNIT(3, it - u_begin);
+        if (dw == kNumDecWarps - 1) SALR_TRACE_UNIT(4, it - u_begin);
+      }
+      s += kDecGroups;
+      while (s >= S) { s -= S; ph ^= 1; }
+    }
+  } else if (warp >= kFirstEpiWarp && warp < kFirstEpiWarp + 4) {
+    // ================= epilogue
+    const int q = warp & 3;
+    const uint32_t lane_tm = (uint32_t)(32 * q) << 16;
+    const int etid = (warp - kFirstEpiWarp) * 32 + (int)lane;  // 0..127
+    const int rp = 64 * p.ra;
+    uint32_t par = 0;
+    if (p.u_mode == 1) {
+      // ---- this CTA's K-slice partial of U = X @ A_cat -> int64 atomics
+      par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
+      unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
+      const int k0 = (int)((int64_t)blockIdx.x * p.K / G), k1 = (int)((int64_t)(blockIdx.x + 1) * p.K / G);
+      const int mh = etid >> 6;
+      for (int a = 0; a < p.ra; ++a) {
+        const int r = 64 * a + (etid & 63);
+        for (int mb = mh; mb < p.M; mb += 16) {
+          float acc[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll 4
+          for (int k = k0; k < k1; ++k) {
+            const float av = __bfloat162float(p.acat[(size_t)k * rp + r]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int m = mb + 2 * i;
+              if (m < p.M) acc[i] = fmaf(__bfloat162float(p.x[(size_t)m * p.ldx + k]), av, acc[i]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int m = mb + 2 * i;
+            if (m < p.M && k1 > k0)
+              atomicAdd(uacc + (size_t)m * rp + r,
+                        (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
+          }
+        }
+      }
+      // the previous adapter launch's buffer (other parity) is idle in this
+      // launch: CTA 0 clears it for the next one
+      if (blockIdx.x == 0) {
+        // the previous user of that buffer may have had another shape: clear
+        // exactly the prefix it recorded as used
+        unsigned long long* other = p.u_acc + (size_t)(par ^ 1u) * kUAccElems;
+        const uint32_t used = p.ctrl[kCtrlUsed + (par ^ 1u)];
+        for (uint32_t i = (uint32_t)etid; i < used; i += 128) other[i] = 0ull;
+        if (etid == 0) {
+          p.ctrl[kCtrlReady + (par ^ 1u)] = 0u;
+          p.ctrl[kCtrlUsed + (par ^ 1u)] = 0u;
+          p.ctrl[kCtrlUsed + par] = (uint32_t)(p.M * rp);
+        }
+      }
+      named_bar_sync(1, 128);
+      if (etid == 0) {
+        __threadfence();
+        atomicAdd(p.ctrl + kCtrlReady + par, 1u);
+      }
+    }
+    bool u_ok = false;
+    uint32_t ad_ph = 0;
+    // adapter operands of the output tile whose first k-unit is useg (a
+    // first-k segment) into the single adapter slot: B_cat^T tile by TMA,
+    // U hi/lo (BM x 64 per rank block, K-major, 128B swizzle) built from the
+    // fixed-point U or loaded by TMA.  Prepared as early as the slot allows
+    // (the MMA only needs it after that segment's k-loop).
+    auto prep_adapter = [&](int useg) {
+      const int nt = (useg / p.n_kt) % p.n_nt;
+      const int mc = useg / (p.n_kt * p.n_nt);
+      // ---- adapter operands of this output tile into the adapter slot:
+      // B_cat^T tile by TMA, U hi/lo (BM x 64 per rank block, K-major, 128B
+      // swizzle) built from the fixed-point U or loaded by TMA.
+      if (etid == 0) {
+        while (!mbar_test_wait(ad_empty, ad_ph ^ 1)) __nanosleep(64);
+      }
+      named_bar_sync(1, 128);
+      if (p.u_mode == 1) {
+        if (!u_ok) {
+          if (etid == 0) {
+            const volatile uint32_t* rdy = p.ctrl + kCtrlReady + par;
+            while (*rdy < (uint32_t)G) __nanosleep(128);
+            __threadfence();
+          }
+          named_bar_sync(1, 128);
+          u_ok = true;
+        }
+        const unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
+        for (int e = etid; e < BM * 32 * p.ra; e += 128) {  // (m, r pair) items
+          const int a = e / (BM * 32);
+          const int m = (e / 32) % BM;
+          const int rr = 2 * (e % 32);  // r within the 64-block
+          const int gm = mc * BM + m;
+          float u0 = 0.f, u1 = 0.f;
+          if (gm < p.M) {
+            const unsigned long long* src = uacc + (size_t)gm * rp + 64 * a + rr;
+            u0 = (float)((double)(long long)__ldcg(src) * (1.0 / (double)(1ll << kUFrac)));
+            u1 = (float)((double)(long long)__ldcg(src + 1) * (1.0 / (double)(1ll << kUFrac)));
+          }
+          const __nv_bfloat16 h0 = __float2bfloat16_rn(u0), h1 = __float2bfloat16_rn(u1);
+          const __nv_bfloat16 l0 = __float2bfloat16_rn(u0 - __bfloat162float(h0));
+          const __nv_bfloat16 l1 = __float2bfloat16_rn(u1 - __bfloat162float(h1));
+          const uint32_t boff = (uint32_t)(m * 128 + (((rr >> 3) ^ (m & 7)) << 4) + 2 * (rr & 7));
+          uint8_t* blk = adbuf + (size_t)a * (kAdTileBytes + 2u * BM * 128u);
+          *reinterpret_cast<__nv_bfloat162*>(blk + kAdTileBytes + boff) = __halves2bfloat162(h0, h1);
+          *reinterpret_cast<__nv_bfloat162*>(blk + kAdTileBytes + BM * 128 + boff) = __halves2bfloat162(l0, l1);
+        }
+        fence_proxy_async_smem();
+      }
+      named_bar_sync(1, 128);
+      if (etid == 0) {
+        if (p.u_mode == 2 && !u_ok) {
+          pdl_wait();  // U hi/lo come from the preceding kernel
+          u_ok = true;
+        }
+        const uint32_t ubytes = p.u_mode == 2 ? 2u * BM * 128u : 0u;
+        mbar_arrive_expect_tx(ad_full, (uint32_t)p.ra * (kAdTileBytes + ubytes));
+        for (int a = 0; a < p.ra; ++a) {
+          uint8_t* blk = adbuf + (size_t)a * (kAdTileBytes + 2u * BM * 128u);
+          tma_2d_g2s(blk, &bmap, 64 * a, nt * kTileN, ad_full);
+          if (p.u_mode == 2) {
+            tma_2d_g2s(blk + kAdTileBytes, &uhimap, 64 * a, mc * BM, ad_full);
+            tma_2d_g2s(blk + kAdTileBytes + BM * 128, &ulomap, 64 * a, mc * BM, ad_full);
+          }
+        }
+      }
+      ad_ph ^= 1;
+    };
+    auto next_first_k = [&](int from) {  // first tile boundary >= from within the range
+      const int t = from % p.n_kt == 0 ? from : from - from % p.n_kt + p.n_kt;
+      return t < u_end ? t : u_end;
+    };
+    int next_ad = p.ra ? next_first_k(u_begin) : u_end;
+    if (next_ad < u_end) {
+      prep_adapter(next_ad);
+      next_ad = next_first_k(next_ad + 1);
+    }
+    int seg = 0;
     int u = u_begin;
     while (u < u_end) {
       const int tile_base = u - u % p.n_kt;
       const int seg_end = min(u_end, tile_base + p.n_kt);
-      const bool first_k = (u == tile_base);
-      const bool full_cover = first_k && (seg_end == tile_base + p.n_kt);
+      const bool full_cover = (u == tile_base) && (seg_end == tile_base + p.n_kt);
       const int nt = (u / p.n_kt) % p.n_nt;
       const int mc = u / (p.n_kt * p.n_nt);
-
-      for (int v = u; v < seg_end; ++v, ++it) {
-        const int s = (int)(it % p.stages);
-        const uint32_t ph = (uint32_t)((it / p.stages) & 1);
-        mbar_wait(&full[s], ph);
-        const uint8_t* rec = recbuf + s * kRecSlot;
-        const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec);
-        const uint32_t* gbits = hdr + 4 + q * kTileK;         // this group's 64 row words
-        const uint16_t* vals = reinterpret_cast<const uint16_t*>(rec + kValOffset);
-        // this warp's RP row words (broadcast loads, all issued up front)
-        uint32_t w[RP];
-#pragma unroll
-        for (int i = 0; i < RP; i += 4) {
-          const uint4 q4 = *reinterpret_cast<const uint4*>(gbits + part * RP + i);
-          w[i] = q4.x; w[i + 1] = q4.y; w[i + 2] = q4.z; w[i + 3] = q4.w;
-        }
-        uint32_t off = q == 0 ? 0u : hdr[q - 1];
-        if (part > 0) {  // values of this group in the rows before this slice
-          uint32_t c = 0u;
-          for (int k = (int)lane; k < part * RP; k += 32) c += __popc(gbits[k]);
-          off += __reduce_add_sync(0xffffffffu, c);
-        }
-        uint32_t packed[ACOLS];
-        const uint16_t* vp = vals + off;  // first value of the current row
-#pragma unroll
-        for (int k2 = 0; k2 < ACOLS; ++k2) {
-          const uint32_t w0 = w[2 * k2], w1 = w[2 * k2 + 1];
-          const uint16_t* vp1 = vp + __popc(w0);
-          uint32_t v0 = 0u, v1 = 0u;
-          if (w0 & lanebit) v0 = vp[__popc(w0 & lt)];
-          if (w1 & lanebit) v1 = vp1[__popc(w1 & lt)];
-          vp = vp1 + __popc(w1);
-          packed[k2] = __byte_perm(v0, v1, 0x5410);
-        }
-        const uint32_t taddr = tmem + lane_tm + kAStageCol + 32 * s + ACOLS * part;
-        tmem_st_cols<ACOLS>(taddr, packed);
-        tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&decoded[s]);
-      }
-
-      if (first_k && p.r_pad > 0) {
-        if (!pdl_done) {
-          pdl_wait();  // U = X @ A_cat comes from the preceding kernel
-          pdl_done = true;
-        }
-        const int ra = p.r_pad / 64;
-        // B_cat^T rows -> TMEM adapter A operand (this warp: lane quarter q, column slice `part`)
-        {
-          const int n = nt * kTileN + 32 * q + lane;
-          const uint32_t* src = reinterpret_cast<const uint32_t*>(p.bcat_t + (size_t)n * p.r_pad);
-          const int cols = p.r_pad / 2;                  // u32 columns of this row
-          const int per = cols / NPART;
-          const uint32_t ad_tm = tmem + lane_tm + kAStageCol + 32 * STAGES + per * part;
-          for (int c = 0; c < per; c += 8) {
-            uint32_t r[8];
-#pragma unroll
-            for (int i = 0; i < 8; i += 4) {
-              const uint4 q4 = __ldg(reinterpret_cast<const uint4*>(src + per * part + c + i));
-              r[i] = q4.x; r[i + 1] = q4.y; r[i + 2] = q4.z; r[i + 3] = q4.w;
-            }
-            tmem_st_cols<8>(ad_tm + c, r);
-          }
-        }
-        // U (fp32) -> bf16 hi/lo, K-major 128B-swizzled B operand tiles in smem
-        {
-          const int pairs = BM * (p.r_pad / 2);
-          for (int i = dw * 32 + (int)lane; i < pairs; i += NDEC * 32) {
-            const int m = i / (p.r_pad / 2);
-            const int r = 2 * (i % (p.r_pad / 2));
-            const int gm = mc * BM + m;
-            float2 uv = make_float2(0.f, 0.f);
-            if (gm < p.M) uv = *reinterpret_cast<const float2*>(p.u + (size_t)gm * p.r_pad + r);
-            const __nv_bfloat16 h0 = __float2bfloat16_rn(uv.x), h1 = __float2bfloat16_rn(uv.y);
-            const __nv_bfloat16 l0 = __float2bfloat16_rn(uv.x - __bfloat162float(h0));
-            const __nv_bfloat16 l1 = __float2bfloat16_rn(uv.y - __bfloat162float(h1));
-            const int a = r / 64, rr = r % 64;
-            const int chunk = (rr * 2) / 16, within = (rr * 2) % 16;
-            const uint32_t boff = (uint32_t)(m * 128 + ((chunk ^ (m & 7)) * 16) + within);
-            __nv_bfloat162 hv = __halves2bfloat162(h0, h1), lv = __halves2bfloat162(l0, l1);
-            *reinterpret_cast<__nv_bfloat162*>(ubuf + (size_t)a * BM * 128 + boff) = hv;
-            *reinterpret_cast<__nv_bfloat162*>(ubuf + (size_t)(ra + a) * BM * 128 + boff) = lv;
-          }
-        }
-        fence_proxy_async_smem();
-        tc_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(ad_ready);
-      }
-
-      // ---- epilogue: accumulator columns [part*BM/NPART, (part+1)*BM/NPART)
-      mbar_wait(acc_full, (uint32_t)(seg & 1));
+      const int b = NACC == 2 ? (seg & 1) : 0;
+      const uint32_t acc_ph = (uint32_t)((NACC == 2 ? seg >> 1 : seg) & 1);
+      // long wait: poll gently so the spinning warps do not steal issue slots
+      while (!mbar_test_wait(&acc_full[b], acc_ph)) __nanosleep(256);
       tc_fence_after();
+      if (etid == 0 && seg == 0) SALR_TRACE(7);
       // partial slot of this CTA: 0 for its first segment, 1 otherwise
       float* part_tile = p.partials + ((size_t)blockIdx.x * 2 + (u == u_begin ? 0 : 1)) * (size_t)BM * kTileN;
-      {
-        constexpr int CPW = BM / NPART;   // columns (tokens) per warp
-        const int nl = 32 * q + (int)lane;
-        const int n = nt * kTileN + nl;
-        const bool n_ok = n < p.N;
-        for (int c0 = 0; c0 < CPW; c0 += 16) {
-          uint32_t r[16];
-          const int col = part * CPW + c0;
-          SALR_TMEM_LD_X16(tmem + lane_tm + kAccCol + col, r);
-          tc_wait_ld();
-          const int lim = CPW < 16 ? CPW : 16;
+      const int nl = 32 * q + (int)lane;
+      const int n = nt * kTileN + nl;
+      const bool n_ok = n < p.N;
+      const int rows = min(BM, p.M - mc * BM);
+#pragma unroll 1
+      for (int c0 = 0; c0 < rows; c0 += 8) {
+        uint32_t r[8];
+        SALR_TMEM_LD_X8(tmem + lane_tm + (uint32_t)(b * ACOLS + c0), r);
+        tc_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (i >= lim) break;
-            const float val = __uint_as_float(r[i]);
-            if (full_cover) {
-              const int m = mc * BM + col + i;
-              if (!n_ok || m >= p.M) continue;
-              if (p.y_dtype == kF32) static_cast<float*>(p.y)[(size_t)m * p.ldy + n] = val;
-              else static_cast<__nv_bfloat16*>(p.y)[(size_t)m * p.ldy + n] = __float2bfloat16_rn(val);
-            } else {
-              __stcg(part_tile + (size_t)(col + i) * kTileN + nl, val);
-            }
+        for (int i = 0; i < 8; ++i) {
+          if (c0 + i >= rows) break;
+          const float val = __uint_as_float(r[i]);
+          if (full_cover) {
+            if (!n_ok) continue;
+            const size_t o = (size_t)(mc * BM + c0 + i) * p.ldy + n;
+            if (p.y_dtype == kF32) static_cast<float*>(p.y)[o] = val;
+            else static_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(val);
+          } else {
+            __stcg(part_tile + (size_t)(c0 + i) * kTileN + nl, val);
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(acc_empty);
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
+      // this segment's adapter (if any) was consumed before acc_full: the
+      // slot is free for the next first-k segment
+      if (next_ad < u_end && u == tile_base) {
+        prep_adapter(next_ad);
+        next_ad = next_first_k(next_ad + 1);
+      }
 
       if (!full_cover) {
         // stream-K fixup: the last CTA to finish this (m-chunk, n-tile) sums
         // the partial tiles of CTAs c_first..c_last in that fixed order.
-        __threadfence();
-        named_bar_sync(1, NDEC * 32);
+        named_bar_sync(1, 128);  // all 128 partial columns stored (CTA scope)
         const int a = tile_base;
         const int c_first = cta_of(a, p.units, G), c_last = cta_of(a + p.n_kt - 1, p.units, G);
-        if (dw == 0 && lane == 0) {
-          const uint32_t old = atomicAdd(&p.tickets[mc * p.n_nt + nt], 1u);
+        if (etid == 0) {
+          // acq_rel at GPU scope publishes this CTA's partial (ordered before
+          // by the CTA barrier + cumulativity) and acquires the others'.
+          const uint32_t old = ticket_add_acq_rel(&p.tickets[mc * p.n_nt + nt], 1u);
           *last_flag = (old + 1 == (uint32_t)(c_last - c_first + 1)) ? 1u : 0u;
         }
-        named_bar_sync(1, NDEC * 32);
+        named_bar_sync(1, 128);
         if (*last_flag) {
-          __threadfence();
-          const int tid = dw * 32 + (int)lane;
-          const int nl = tid % kTileN;
-          const int n = nt * kTileN + nl;
-          for (int mm = tid / kTileN; mm < BM; mm += NDEC * 32 / kTileN) {
-            const int m = mc * BM + mm;
-            if (m >= p.M || n >= p.N) continue;
-            float acc = 0.0f;
+          // thread etid owns column n2; rows in register chunks of 16 so all
+          // loads of one partial tile are in flight together.  Summation order
+          // per element is c_first..c_last (deterministic).
+          const int n2 = nt * kTileN + etid;
+          for (int m0 = 0; m0 < rows; m0 += 16) {
+            float acc[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
             for (int c = c_first; c <= c_last; ++c) {
               const int cb = (int)((int64_t)c * p.units / G);  // u_begin of CTA c
-              const float* pt = p.partials + ((size_t)c * 2 + (cb >= a ? 0 : 1)) * (size_t)BM * kTileN;
-              acc += __ldcg(pt + (size_t)mm * kTileN + nl);
+              const float* pt = p.partials + ((size_t)c * 2 + (cb >= a ? 0 : 1)) * (size_t)BM * kTileN +
+                                (size_t)m0 * kTileN + etid;
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (m0 + i < rows) acc[i] += __ldcg(pt + (size_t)i * kTileN);
             }
-            if (p.y_dtype == kF32) static_cast<float*>(p.y)[(size_t)m * p.ldy + n] = acc;
-            else static_cast<__nv_bfloat16*>(p.y)[(size_t)m * p.ldy + n] = __float2bfloat16_rn(acc);
+            if (n2 < p.N) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                if (m0 + i >= rows) break;
+                const size_t o = (size_t)(mc * BM + m0 + i) * p.ldy + n2;
+                if (p.y_dtype == kF32) static_cast<float*>(p.y)[o] = acc[i];
+                else static_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(acc[i]);
+              }
+            }
           }
-          if (tid == 0) p.tickets[mc * p.n_nt + nt] = 0u;
+          if (etid == 0) p.tickets[mc * p.n_nt + nt] = 0u;
         }
-        named_bar_sync(1, NDEC * 32);
+        named_bar_sync(1, 128);
       }
       ++seg;
       u = seg_end;
     }
+    if (etid == 0) SALR_TRACE(8);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == kWarpMma) {
     tc_fence_after();
-    tmem_dealloc(tmem, kTmemCols);
+    if (lane == 0) SALR_TRACE(9);
+    tmem_dealloc(tmem, 512);
+  }
+  if (p.u_mode == 1 && threadIdx.x == 0) {
+    // the last CTA of this launch advances the epoch (flips the U parity)
+    const uint32_t old = ticket_add_acq_rel(p.ctrl + kCtrlDone, 1u);
+    if (old + 1 == (uint32_t)G) {
+      p.ctrl[kCtrlDone] = 0u;
+      __threadfence();
+      p.ctrl[kCtrlEpoch] = p.ctrl[kCtrlEpoch] + 1u;
+    }
   }
 }
 
-// U[m, r] = sum_k X[m, k] * A_cat[k, r] (fp32).  Grid (m-blocks of 8 rows,
-// K splits, r blocks of 64); every block stores its partial, and the last
-// block of each (m-block, r-block) -- found with a self-resetting ticket --
-// sums the K-split partials in split order, so U is bit-reproducible.
+// U[m, r] = sum_k X[m, k] * A_cat[k, r] (fp32), written as bf16 hi + lo
+// halves (U = hi + lo to ~2^-16 relative).  Grid (m-blocks of 8 rows, K
+// splits, r blocks of 64); every block stores its partial, and the last block
+// of each (m-block, r-block) -- found with a self-resetting ticket -- sums
+// the K-split partials in split order, so U is bit-reproducible.
 __global__ void __launch_bounds__(256) adapter_u_kernel(const __nv_bfloat16* __restrict__ x, int64_t M, int64_t K,
                                                         int64_t ldx, const __nv_bfloat16* __restrict__ acat,
                                                         int r_pad, int64_t kchunk, float* __restrict__ u_part,
-                                                        uint32_t* __restrict__ u_tickets, float* __restrict__ u) {
+                                                        uint32_t* __restrict__ u_tickets,
+                                                        __nv_bfloat16* __restrict__ u_hi,
+                                                        __nv_bfloat16* __restrict__ u_lo) {
   pdl_launch_dependents();
   constexpr int MB = 8;
   __shared__ uint32_t is_last;
@@ -447,7 +753,9 @@ __global__ void __launch_bounds__(256) adapter_u_kernel(const __nv_bfloat16* __r
     if (m >= M) continue;
     float sum = 0.f;
     for (unsigned ks = 0; ks < gridDim.y; ++ks) sum += __ldcg(u_part + (size_t)ks * M * r_pad + m * r_pad + r);
-    u[m * r_pad + r] = sum;
+    const __nv_bfloat16 h = __float2bfloat16_rn(sum);
+    u_hi[m * r_pad + r] = h;
+    u_lo[m * r_pad + r] = __float2bfloat16_rn(sum - __bfloat162float(h));
   }
   if (threadIdx.x == 0 && ty == 0) *ticket = 0u;
 }
@@ -480,15 +788,58 @@ static int sm_count() {
   return n;
 }
 
-template <int BM>
-static int launch_linear(const CUtensorMap& xmap, const LinearParams& p, int ctas, cudaStream_t s, bool pdl) {
-  constexpr int NDEC = 16;
-  auto kern = salr_linear_kernel<BM, NDEC>;
-  const SmemPlan plan = smem_plan(BM, stages_for(BM), p.r_pad);
-  SALR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.total));
+// bf16 2-D tensor map over a row-major (rows x cols) matrix, box (64 cols, box_rows), 128B swizzle.
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld_elems,
+                    int box_rows) {
+  EncodeTiledFn enc = get_encode_tiled();
+  SALR_CHECK_ARG(enc != nullptr, SALR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld_elems * 2};
+  const cuuint32_t box[2] = {64u, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult cr = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SALR_CHECK_ARG(cr == CUDA_SUCCESS, SALR_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
+  return SALR_OK;
+}
+
+static unsigned long long* g_trace = nullptr;  // set by salr_debug_set_trace (tools only)
+
+static int pick_bm(int64_t M) {
+  if (M <= 16) return 16;
+  if (M <= 32) return 32;
+  if (M <= 64) return 64;
+  return 128;
+}
+
+// deepest ring that fits shared memory and TMEM
+static int max_stages(int bm, int ra) {
+  const int acc = nacc_for(bm) * acc_cols_for(bm);
+  const int tmem_stages = (512 - ((acc + 31) & ~31)) / 32;
+  int s = 8;
+  if (s > tmem_stages) s = tmem_stages;
+  while (s > 1 && smem_plan(bm, s, ra).total > kSmemMax) --s;
+  return s;
+}
+
+template <int BM, int NG>
+static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cudaStream_t s, bool pdl) {
+  auto kern = salr_linear_kernel<BM, NG>;
+  const SmemPlan plan = smem_plan(BM, p.stages, p.ra);
+  p.x_off = plan.x_off;
+  p.rec_off = plan.rec_off;
+  p.base_off = plan.base_off;
+  p.ad_off = plan.ad_off;
+  p.bar_off = plan.bar_off;
+  static bool attr_done = false;
+  if (!attr_done) {
+    SALR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    attr_done = true;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctas);
-  cfg.blockDim = dim3(128 + NDEC * 32);
+  cfg.blockDim = dim3(kNumThreads);
   cfg.dynamicSmemBytes = plan.total;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -496,28 +847,43 @@ static int launch_linear(const CUtensorMap& xmap, const LinearParams& p, int cta
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  SALR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, xmap, p));
+  SALR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p));
   return SALR_OK;
+}
+
+static int dec_groups() {
+  static int g = 0;
+  if (!g) {
+    const char* e = getenv("SALR_DEC_GROUPS");
+    g = e ? atoi(e) : 4;
+    if (g != 1 && g != 2 && g != 4) g = 4;
+  }
+  return g;
+}
+
+template <int BM>
+static int launch_linear(const CUtensorMap* maps, const LinearParams& p, int ctas, cudaStream_t s, bool pdl) {
+  switch (dec_groups()) {
+    case 1: return launch_linear_g<BM, 1>(maps, p, ctas, s, pdl);
+    case 2: return launch_linear_g<BM, 2>(maps, p, ctas, s, pdl);
+    default: return launch_linear_g<BM, 4>(maps, p, ctas, s, pdl);
+  }
 }
 
 static inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
-static int pick_bm(int64_t M) {
-  if (M <= 16) return 16;
-  if (M <= 32) return 32;
-  if (M <= 64) return 64;
-  if (M <= 128) return 128;
-  return 256;
-}
-
 // Workspace layout.  The first kTicketBytes hold the self-resetting ticket
 // counters at FIXED offsets (tile tickets, then U tickets) so that calls with
 // different shapes sharing one workspace never see stale scratch data there;
-// the scratch regions (U, U k-split partials, split-K partial tiles) follow.
+// the scratch regions (U hi/lo, U k-split partials, split-K partial tiles)
+// follow.
 constexpr size_t kTicketBytes = 256 * 1024;
-constexpr int64_t kMaxTileTickets = 32 * 1024, kMaxUTickets = 32 * 1024;
+constexpr int64_t kMaxTileTickets = 32 * 1024, kMaxUTickets = 16 * 1024;
+constexpr size_t kCtrlOff = kTicketBytes - 64;                 // adapter control words
+constexpr size_t kUAccOff = kTicketBytes;                      // 2 parity buffers, fixed place
+constexpr size_t kUAccBytes = 2 * (size_t)kUAccElems * 8;
 struct WsLayout {
-  size_t u, u_part, u_tickets, partials, tickets, total;
+  size_t u_hi, u_lo, u_part, u_tickets, partials, tickets, total;
   int64_t mblocks, ksplit, kchunk, n_tile_tickets;
 };
 static WsLayout ws_layout(int64_t M, int64_t N, int64_t K, int64_t r_pad, int64_t ctas) {
@@ -533,9 +899,11 @@ static WsLayout ws_layout(int64_t M, int64_t N, int64_t K, int64_t r_pad, int64_
   w.ksplit = (K + w.kchunk - 1) / w.kchunk;
   w.tickets = 0;
   w.u_tickets = kTicketBytes / 2;
-  size_t off = kTicketBytes;
-  w.u = off;
-  off += align256((size_t)M * r_pad * 4);
+  size_t off = kUAccOff + kUAccBytes;
+  w.u_hi = off;
+  off += align256((size_t)M * r_pad * 2);
+  w.u_lo = off;
+  off += align256((size_t)M * r_pad * 2);
   w.u_part = off;
   off += r_pad ? align256((size_t)w.ksplit * M * r_pad * 4) : 0;
   w.partials = off;
@@ -549,6 +917,13 @@ static WsLayout ws_layout(int64_t M, int64_t N, int64_t K, int64_t r_pad, int64_
 using namespace salr;
 
 extern "C" {
+
+// Timing instrumentation (tools/trace_linear.py): subsequent launches write
+// per-CTA globaltimer stamps into buf[G][32] (u64).  NULL disables.
+int salr_debug_set_trace(void* buf) {
+  g_trace = static_cast<unsigned long long*>(buf);
+  return SALR_OK;
+}
 
 size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pad, int num_ctas) {
   return ws_layout(M, N, K, r_pad, num_ctas > 0 ? num_ctas : sm_count()).total;
@@ -571,24 +946,19 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
                  "workspace too small (%zu < %zu)", workspace_bytes,
                  salr_linear_workspace_bytes(M, N, K, r_pad, num_ctas));
   const int bm = pick_bm(M);
-  SALR_CHECK_ARG(!(bm == 256 && r_pad > 64), SALR_ERR_CONFIG, "r_pad=128 needs M <= 128 per chunk");
-  {
-    const WsLayout w0 = ws_layout(M, N, K, r_pad, num_ctas > 0 ? num_ctas : sm_count());
-    SALR_CHECK_ARG(w0.n_tile_tickets <= kMaxTileTickets && w0.mblocks * 2 <= kMaxUTickets, SALR_ERR_CONFIG,
-                   "problem too large for the ticket area (%lld tiles, %lld m-blocks)",
-                   (long long)w0.n_tile_tickets, (long long)w0.mblocks);
-  }
-  EncodeTiledFn enc = get_encode_tiled();
-  SALR_CHECK_ARG(enc != nullptr, SALR_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int ra = (int)(r_pad / 64);
+  const WsLayout wl = ws_layout(M, N, K, r_pad, num_ctas > 0 ? num_ctas : sm_count());
+  SALR_CHECK_ARG(wl.n_tile_tickets <= kMaxTileTickets && wl.mblocks * 2 <= kMaxUTickets, SALR_ERR_CONFIG,
+                 "problem too large for the ticket area (%lld tiles, %lld m-blocks)", (long long)wl.n_tile_tickets,
+                 (long long)wl.mblocks);
+  SALR_CHECK_ARG(M * (ldy > N ? ldy : N) < ((int64_t)1 << 31) && M * r_pad < ((int64_t)1 << 31), SALR_ERR_SHAPE,
+                 "M x N = %lld x %lld exceeds the 32-bit output index", (long long)M, (long long)N);
 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   LinearParams p = {};
   p.records = records;
   p.tile_off = tile_off;
-  p.bcat_t = static_cast<const __nv_bfloat16*>(bcat_t);
   p.y = y;
-  SALR_CHECK_ARG(M * (ldy > N ? ldy : N) < ((int64_t)1 << 31) && M * r_pad < ((int64_t)1 << 31), SALR_ERR_SHAPE,
-                 "M x N = %lld x %lld exceeds the 32-bit output index", (long long)M, (long long)N);
   p.M = (int)M;
   p.N = (int)N;
   p.ldy = (int)ldy;
@@ -597,47 +967,65 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   p.n_mc = (int)((M + bm - 1) / bm);
   SALR_CHECK_ARG((int64_t)p.n_mc * p.n_nt * p.n_kt < ((int64_t)1 << 31), SALR_ERR_SHAPE, "too many work units");
   p.units = p.n_mc * p.n_nt * p.n_kt;
-  p.r_pad = (int)r_pad;
+  p.ra = ra;
   p.y_dtype = y_dtype;
   {
-    const int smax = stages_for(bm);
+    static int dbg = -1;
+    if (dbg < 0) {
+      const char* e = getenv("SALR_DEBUG_MODE");
+      dbg = e ? atoi(e) : 0;
+    }
+    p.dbg = dbg;
+    p.trace = g_trace;
+  }
+  {
+    const int smax = max_stages(bm, ra);
     p.stages = stages <= 0 || stages > smax ? smax : stages;
   }
-  const WsLayout wl = ws_layout(M, N, K, r_pad, num_ctas > 0 ? num_ctas : sm_count());
   uint8_t* ws = static_cast<uint8_t*>(workspace);
-  float* u = reinterpret_cast<float*>(ws + wl.u);
   p.partials = reinterpret_cast<float*>(ws + wl.partials);
   p.tickets = reinterpret_cast<uint32_t*>(ws + wl.tickets);
-  p.u = r_pad ? u : nullptr;
+  __nv_bfloat16* u_hi = reinterpret_cast<__nv_bfloat16*>(ws + wl.u_hi);
+  __nv_bfloat16* u_lo = reinterpret_cast<__nv_bfloat16*>(ws + wl.u_lo);
 
-  CUtensorMap xmap;
-  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
-  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)kTileK, (cuuint32_t)bm};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult cr = enc(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, estr,
-                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  SALR_CHECK_ARG(cr == CUDA_SUCCESS, SALR_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)cr);
-
-  bool pdl = false;
-  if (r_pad) {
-    adapter_u_kernel<<<dim3((unsigned)wl.mblocks, (unsigned)wl.ksplit, (unsigned)(r_pad / 64)), dim3(64, 4), 0, s>>>(
-        static_cast<const __nv_bfloat16*>(x), M, K, ldx, static_cast<const __nv_bfloat16*>(acat), (int)r_pad,
-        wl.kchunk, reinterpret_cast<float*>(ws + wl.u_part), reinterpret_cast<uint32_t*>(ws + wl.u_tickets), u);
-    SALR_LAUNCH_CHECK();
-    pdl = true;
+  CUtensorMap maps[4];
+  int rc = make_map(&maps[0], x, M, K, ldx, bm);
+  if (rc) return rc;
+  if (ra) {
+    const int64_t n_pad = (int64_t)p.n_nt * kTileN;
+    if ((rc = make_map(&maps[1], bcat_t, n_pad, r_pad, r_pad, kTileN))) return rc;
+    if ((rc = make_map(&maps[2], u_hi, M, r_pad, r_pad, bm))) return rc;
+    if ((rc = make_map(&maps[3], u_lo, M, r_pad, r_pad, bm))) return rc;
+  } else {
+    maps[1] = maps[2] = maps[3] = maps[0];
   }
+
   int64_t ctas = num_ctas > 0 ? num_ctas : sm_count();
   if (ctas > p.units) ctas = p.units;
   SALR_CHECK_ARG(ctas <= 65535, SALR_ERR_CONFIG, "num_ctas too large");
-  int rc;
+  // in-kernel U needs every CTA resident at once (they wait on each other's
+  // partials): one CTA per SM, grid <= SM count
+  p.u_mode = ra ? ((M <= 256 && ctas <= sm_count()) ? 1 : 2) : 0;
+  p.K = (int)K;
+  p.x = static_cast<const __nv_bfloat16*>(x);
+  p.acat = static_cast<const __nv_bfloat16*>(acat);
+  p.ldx = (int)ldx;
+  p.u_acc = reinterpret_cast<unsigned long long*>(ws + kUAccOff);
+  p.ctrl = reinterpret_cast<uint32_t*>(ws + kCtrlOff);
+  bool pdl = false;
+  if (p.u_mode == 2) {
+    adapter_u_kernel<<<dim3((unsigned)wl.mblocks, (unsigned)wl.ksplit, (unsigned)ra), dim3(64, 4), 0, s>>>(
+        static_cast<const __nv_bfloat16*>(x), M, K, ldx, static_cast<const __nv_bfloat16*>(acat), (int)r_pad,
+        wl.kchunk, reinterpret_cast<float*>(ws + wl.u_part), reinterpret_cast<uint32_t*>(ws + wl.u_tickets), u_hi,
+        u_lo);
+    SALR_LAUNCH_CHECK();
+    pdl = true;
+  }
   switch (bm) {
-    case 16: rc = launch_linear<16>(xmap, p, (int)ctas, s, pdl); break;
-    case 32: rc = launch_linear<32>(xmap, p, (int)ctas, s, pdl); break;
-    case 64: rc = launch_linear<64>(xmap, p, (int)ctas, s, pdl); break;
-    case 128: rc = launch_linear<128>(xmap, p, (int)ctas, s, pdl); break;
-    default: rc = launch_linear<256>(xmap, p, (int)ctas, s, pdl); break;
+    case 16: rc = launch_linear<16>(maps, p, (int)ctas, s, pdl); break;
+    case 32: rc = launch_linear<32>(maps, p, (int)ctas, s, pdl); break;
+    case 64: rc = launch_linear<64>(maps, p, (int)ctas, s, pdl); break;
+    default: rc = launch_linear<128>(maps, p, (int)ctas, s, pdl); break;
   }
   return rc;
 }
