@@ -294,22 +294,22 @@ class StackRunner:
             outs = {}
             for name in ("q", "k", "v"):
                 s, f, _, _ = lin[name]
-                outs[name] = S.salr_linear(h, s, f, out=self.bufs[name], check_finite=False)
+                outs[name] = S.salr_linear(h, s, f, out=self.bufs[name], check_finite=False, pdl=True)
                 launches += 2
             q, _, _ = self._gather([outs["q"], outs["k"], outs["v"]], [4096, 1024, 1024])
             s, f, _, _ = lin["o"]
-            o = S.salr_linear(q, s, f, out=self.bufs["o"], check_finite=False)
+            o = S.salr_linear(q, s, f, out=self.bufs["o"], check_finite=False, pdl=True)
             launches += 2
             (o,) = self._gather([o], [4096])
             for name in ("gate", "up"):
                 s, f, _, _ = lin[name]
-                outs[name] = S.salr_linear(o, s, f, out=self.bufs[name], check_finite=False)
+                outs[name] = S.salr_linear(o, s, f, out=self.bufs[name], check_finite=False, pdl=True)
                 launches += 2
             # the stack is linears only (the MLP nonlinearity is outside the hot
             # path): down consumes the gathered gate projection
             gate, _ = self._gather([outs["gate"], outs["up"]], [14336, 14336])
             s, f, _, _ = lin["down"]
-            d = S.salr_linear(gate, s, f, out=self.bufs["down"], check_finite=False)
+            d = S.salr_linear(gate, s, f, out=self.bufs["down"], check_finite=False, pdl=True)
             launches += 2
             (h,) = self._gather([d], [4096])
         self.launches_per_step = launches
@@ -341,32 +341,52 @@ def time_steps(fn, steps, warmup, world, sampler_dev):
     return ms, cs.summary()
 
 
-def per_linear_kernel_times(stack, tokens, reps=20):
-    """Average device time of each linear's launch (U pre-kernel + fused kernel),
-    CUDA events on the launching stream, layers rotated to defeat L2."""
+def graph_time_us(fn, reps):
+    """Device time per call of `fn(i)`: one CUDA graph of `reps` back-to-back
+    calls, best of 3 replays timed with CUDA events on the capture stream."""
+    import torch
+    fn(0)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            fn(i)
+    g.replay()
+    torch.cuda.synchronize()
+    best = None
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        e1.synchronize()
+        t = 1e3 * e0.elapsed_time(e1) / reps
+        best = t if best is None else min(best, t)
+    del g
+    return best
+
+
+def per_linear_kernel_times(stack, tokens, reps=32):
+    """Device time of each linear (the fused kernel; launched back to back
+    with programmatic dependent launch as in the stack), layers rotated so
+    every launch streams its weights from HBM."""
     import torch
     import paper_2601_16991_b200 as S
     res = {}
     x = {4096: torch.randn(tokens, 4096, device="cuda").bfloat16(),
          14336: torch.randn(tokens, 14336, device="cuda").bfloat16()}
+    L = len(stack)
     for name in LINEARS:
         k, nl = stack[0][name][2]
-        out = torch.empty(tokens, nl, dtype=torch.bfloat16, device="cuda")
-        L = len(stack)
-        for i in range(3):
+        outs = [torch.empty(tokens, nl, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
+
+        def call(i):
             s, f, _, _ = stack[i % L][name]
-            S.salr_linear(x[k], s, f, out=out, check_finite=False)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(reps):
-            s, f, _, _ = stack[i % L][name]
-            S.salr_linear(x[k], s, f, out=out, check_finite=False)
-        e1.record()
-        e1.synchronize()
+            S.salr_linear(x[k], s, f, out=outs[i & 1], check_finite=False, pdl=True)
+
+        us = graph_time_us(call, reps)
         s0 = stack[0][name][0]
-        res[name] = {"us": 1e3 * e0.elapsed_time(e1) / reps, "compressed_bytes": s0.compressed_bytes,
-                     "nnz": s0.nnz, "shape": [k, nl]}
+        res[name] = {"us": us, "compressed_bytes": s0.compressed_bytes, "nnz": s0.nnz, "shape": [k, nl]}
     return res
 
 
@@ -383,16 +403,8 @@ def cublas_times(stack, tokens, reps=20):
             s, f, _, _ = stack[i][name]
             ws.append((S.decode(s) + f.a_cat @ f.b_cat).bfloat16())
         x = torch.randn(tokens, k, device="cuda").bfloat16()
-        for i in range(3):
-            torch.matmul(x, ws[i % L])
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for i in range(reps):
-            torch.matmul(x, ws[i % L])
-        e1.record()
-        e1.synchronize()
-        res[name] = {"us": 1e3 * e0.elapsed_time(e1) / reps, "dense_bytes": 2 * k * nl}
+        us = graph_time_us(lambda i: torch.matmul(x, ws[i % L]), reps)
+        res[name] = {"us": us, "dense_bytes": 2 * k * nl}
         del ws
         torch.cuda.empty_cache()
     return res

@@ -123,10 +123,16 @@ size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pa
  * write per-CTA %globaltimer stamps of pipeline events into buf[cta][32]
  * (u64, device memory, >= 32 * 8 * num_ctas bytes).  NULL disables. */
 int salr_debug_set_trace(void* buf);
+/* flags: SALR_FLAG_PDL launches the kernel as a programmatic dependent of the
+ * preceding work on the stream: its weight-streaming prologue overlaps the
+ * tail of that work and it waits for it (griddepcontrol.wait) before reading
+ * x.  The caller must not let the preceding kernel still READ y, and must use
+ * a workspace the preceding kernel does not use (alternate two). */
+#define SALR_FLAG_PDL 1
 int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const uint8_t* records,
                         const uint32_t* tile_off, int64_t N, const void* acat, const void* bcat_t,
                         int64_t r_pad, void* y, int y_dtype, int64_t ldy, void* workspace,
-                        size_t workspace_bytes, int stages, int num_ctas, void* stream);
+                        size_t workspace_bytes, int stages, int num_ctas, int flags, void* stream);
 
 #ifdef __cplusplus
 }

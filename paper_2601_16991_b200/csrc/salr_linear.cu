@@ -38,6 +38,7 @@
 //     stores its fp32 partial tile and the last CTA to finish that tile sums
 //     the partials in a fixed CTA order -- results are bit-identical from run
 //     to run (the reference's schedule independence, test_pipeline.py:90-112).
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda.h>
@@ -181,6 +182,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   if (threadIdx.x == 0) SALR_TRACE(10);
+  // let the next kernel in the stream start its weight-only prologue as soon
+  // as SMs free up (it waits for this grid before touching our output)
+  if (threadIdx.x == 0) pdl_launch_dependents();
   if (threadIdx.x == 0 && p.trace && blockIdx.x == 0) p.trace[148 * 32 + 7 * 64] = clock64();
 
   // ---- per-CTA work range
@@ -192,12 +196,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // ---- producer state (warps kWarpProd0 / kWarpProd1, units of one parity).
   // Record offsets are fetched 32 units at a time, one chunk ahead, one
   // coalesced load per lane, so the issue loop never waits on a global load.
+  // Each multi-instance role owns the stages s = instance (mod instances), so
+  // an instance never waits on a stage two phases ahead (mbarrier parity
+  // waits cannot tell those apart): the host picks S as a multiple of the
+  // decoder group count, and the producers / row-base warps run as pairs only
+  // when S is even.
+  const int NP = (S % 2 == 0) ? 2 : 1;
   const int pk = warp == kWarpProd1 ? 1 : 0;
   uint32_t co0 = 0, co1 = 0, no0 = 0, no1 = 0;
   int chunk = u_begin;
   int pv = u_begin + pk;  // next unit to issue (this producer's parity)
-  int ps = pk % S;
-  uint32_t pph = (uint32_t)((pk / S) & 1);
+  int ps = pk;            // < S whenever this producer is active
+  uint32_t pph = 0;
   auto load_chunk = [&](int c0, uint32_t& o0, uint32_t& o1) {
     const int v = c0 + (int)lane;
     o0 = o1 = 0u;
@@ -207,7 +217,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       o1 = __ldg(p.tile_off + t + 1);
     }
   };
-  auto issue_one = [&]() {
+  // X tile of unit v into stage st (the input; may have to wait for the
+  // preceding kernel under programmatic dependent launch)
+  auto issue_x = [&](int v, int st) {
+    const int kt = v % p.n_kt;
+    const int mc = v / tiles_per_mc;
+    tma_2d_g2s(xbuf + (size_t)st * BM * 128, &xmap, kt * kTileK, mc * BM, &full[st]);
+  };
+  // Issue unit pv.  The copies go out before arrive.expect_tx (the phase
+  // cannot complete before the arrive, and issuing the copy first keeps it
+  // off the arrive's latency).  The first ring's worth of units never waits
+  // for `empty`.  with_x = false defers the X tile (see the PDL prologue).
+  auto issue_one = [&](bool with_x) {
     while (pv - chunk >= 32) {
       chunk += 32;
       co0 = no0;
@@ -216,26 +237,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     const uint32_t o0 = __shfl_sync(0xffffffffu, co0, pv - chunk);
     const uint32_t o1 = __shfl_sync(0xffffffffu, co1, pv - chunk);
-    mbar_wait(&empty[ps], pph ^ 1);
+    if (pv - u_begin >= S) mbar_wait(&empty[ps], pph ^ 1);
     if (lane == 0) {
-      const int kt = pv % p.n_kt;
-      const int mc = pv / tiles_per_mc;
-      const uint32_t bytes = (o1 - o0) * 16u;
-      if (p.dbg & 2) {
-        mbar_arrive_expect_tx(&full[ps], BM * 128);
-      } else {
-        mbar_arrive_expect_tx(&full[ps], bytes + BM * 128);
-        bulk_g2s(recbuf + (size_t)ps * kRecSlot, p.records + (size_t)o0 * 16u, bytes, &full[ps]);
-      }
-      tma_2d_g2s(xbuf + (size_t)ps * BM * 128, &xmap, kt * kTileK, mc * BM, &full[ps]);
+      const uint32_t bytes = (p.dbg & 2) ? 0u : (o1 - o0) * 16u;
+      if (bytes) bulk_g2s(recbuf + (size_t)ps * kRecSlot, p.records + (size_t)o0 * 16u, bytes, &full[ps]);
+      if (with_x) issue_x(pv, ps);
+      mbar_arrive_expect_tx(&full[ps], bytes + BM * 128);
       SALR_TRACE_UNIT(0, pv - u_begin);
     }
     __syncwarp();
-    ps += 2;
-    while (ps >= S) { ps -= S; pph ^= 1; }
-    pv += 2;
+    ps += NP;
+    if (ps >= S) { ps -= S; pph ^= 1; }
+    pv += NP;
   };
 
+  const bool producer = warp == kWarpProd0 || (warp == kWarpProd1 && NP == 2);
   if (warp == kWarpProd0 || warp == kWarpProd1) {
     load_chunk(u_begin, co0, co1);
     load_chunk(u_begin + 32, no0, no1);
@@ -265,7 +281,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // of the first ring's worth of units of the first output tile (never blocks).
     const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
     const int pre = min(first_seg_end, u_begin + S);
-    while (pv < pre) issue_one();
+    const int pv0 = pv;
+    if (producer)
+      while (pv < pre) issue_one(false);
+    // Weights never depend on the preceding kernel; the input X may (it can
+    // be that kernel's output).  Wait for it only now, then send the X tiles
+    // of the units already in flight.
+    pdl_wait();
+    if (lane == 0 && producer)
+      for (int v = pv0; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
+    __syncwarp();
   }
   if (warp == kWarpMma) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
@@ -278,25 +303,27 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (warp == kWarpProd0 || warp == kWarpProd1) {
     // ================= TMA producers
     if (lane == 0 && pk == 0) SALR_TRACE(1);
-    while (pv < u_end) issue_one();
+    if (producer)
+      while (pv < u_end) issue_one(true);
     if (lane == 0 && pk == 0) SALR_TRACE(2);
   } else if (warp == kWarpMma) {
-    // ================= MMA issuer (one thread)
-    if (lane == 0) {
-      int s = 0, seg = 0;
-      uint32_t ph = 0, ad_ph = 0;
-      int u = u_begin;
-      while (u < u_end) {
-        const int tile_base = u - u % p.n_kt;
-        const int seg_end = min(u_end, tile_base + p.n_kt);
-        const int b = NACC == 2 ? (seg & 1) : 0;
-        const uint32_t acc_ph = (uint32_t)((NACC == 2 ? seg >> 1 : seg) & 1);
-        const uint32_t acc = tmem + (uint32_t)(b * ACOLS);
-        mbar_wait(&acc_empty[b], acc_ph ^ 1);
+    // ================= MMA issuer: the whole warp walks the schedule (warp-
+    // uniform state stays in uniform registers); one elected lane issues.
+    int s = 0, seg = 0;
+    uint32_t ph = 0, ad_ph = 0;
+    int u = u_begin;
+    while (u < u_end) {
+      const int tile_base = u - u % p.n_kt;
+      const int seg_end = min(u_end, tile_base + p.n_kt);
+      const int b = NACC == 2 ? (seg & 1) : 0;
+      const uint32_t acc_ph = (uint32_t)((NACC == 2 ? seg >> 1 : seg) & 1);
+      const uint32_t acc = tmem + (uint32_t)(b * ACOLS);
+      mbar_wait(&acc_empty[b], acc_ph ^ 1);
+      tc_fence_after();
+      for (int v = u; v < seg_end; ++v) {
+        mbar_wait(&decoded[s], ph);
         tc_fence_after();
-        for (int v = u; v < seg_end; ++v) {
-          mbar_wait(&decoded[s], ph);
-          tc_fence_after();
+        if (elect_one()) {
           const uint64_t bdesc = desc_kmajor_sw128(smem_u32(xbuf + (size_t)s * BM * 128));
           const uint32_t a_tm = tmem + a_col0 + 32u * s;
 #pragma unroll
@@ -305,12 +332,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           tc_commit(&empty[s]);
           if (v == u_begin) SALR_TRACE(5);
           SALR_TRACE_UNIT(5, v - u_begin);
-          if (++s == S) { s = 0; ph ^= 1; }
         }
-        if (u == tile_base && p.ra) {
-          mbar_wait(ad_full, ad_ph);
-          ad_ph ^= 1;
-          tc_fence_after();
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1; }
+      }
+      if (u == tile_base && p.ra) {
+        mbar_wait(ad_full, ad_ph);
+        ad_ph ^= 1;
+        tc_fence_after();
+        if (elect_one()) {
           for (int a = 0; a < p.ra; ++a) {
             uint8_t* blk = adbuf + (size_t)a * (kAdTileBytes + 2u * BM * 128u);
             const uint64_t adesc = desc_kmajor_sw128(smem_u32(blk));
@@ -323,11 +353,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
           tc_commit(ad_empty);
         }
+        __syncwarp();
+      }
+      if (elect_one()) {
         tc_commit(&acc_full[b]);
         SALR_TRACE(6);
-        ++seg;
-        u = seg_end;
       }
+      __syncwarp();
+      ++seg;
+      u = seg_end;
     }
   } else if (warp == kWarpPrep0 || warp == kWarpPrep1) {
     // ================= row bases (two warps, alternate units): exclusive
@@ -335,9 +369,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // the shared-memory byte address where each (group, row) value run starts.
     // lane l handles rows 2l, 2l+1 of all four groups.
     const int w2 = warp - kWarpPrep0;
-    int s = w2 % S;
-    uint32_t ph = (uint32_t)((w2 / S) & 1);
-    for (int it = u_begin + w2; it < u_end; it += 2) {
+    int s = w2;
+    uint32_t ph = 0;
+    for (int it = u_begin + w2; it < u_end && (w2 < NP); it += NP) {
       mbar_wait(&full[s], ph);
       if (lane == 0) SALR_TRACE_UNIT(1, it - u_begin);
       const uint8_t* rec = recbuf + (size_t)s * kRecSlot;
@@ -380,8 +414,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         SALR_TRACE(it == u_begin ? 3 : 12);
         SALR_TRACE_UNIT(2, it - u_begin);
       }
-      s += 2;
-      while (s >= S) { s -= S; ph ^= 1; }
+      s += NP;
+      if (s >= S) { s -= S; ph ^= 1; }
     }
   } else if (warp >= kFirstDecWarp && warp < kFirstEpiWarp) {
     // ================= decoders.  Group g = units it = g (mod kDecGroups);
@@ -395,8 +429,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const uint32_t lanebit = 1u << lane;
     const uint32_t lane_tm = (uint32_t)(32 * q) << 16;
     const uint32_t raw_u32 = smem_u32(smem_raw);
-    int s = grp % S;
-    uint32_t ph = (uint32_t)((grp / S) & 1);
+    int s = grp;  // S is a multiple of kDecGroups (host)
+    uint32_t ph = 0;
     for (int it = u_begin + grp; it < u_end; it += kDecGroups) {
       mbar_wait(&full[s], ph);
       mbar_wait(&prepd[s], ph);
@@ -439,7 +473,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (dw == kNumDecWarps - 1) SALR_TRACE_UNIT(4, it - u_begin);
       }
       s += kDecGroups;
-      while (s >= S) { s -= S; ph ^= 1; }
+      if (s >= S) { s -= S; ph ^= 1; }
     }
   } else if (warp >= kFirstEpiWarp && warp < kFirstEpiWarp + 4) {
     // ================= epilogue
@@ -450,6 +484,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint32_t par = 0;
     if (p.u_mode == 1) {
       // ---- this CTA's K-slice partial of U = X @ A_cat -> int64 atomics
+      pdl_wait();  // X may be the preceding kernel's output
       par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
       unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
       const int k0 = (int)((int64_t)blockIdx.x * p.K / G), k1 = (int)((int64_t)(blockIdx.x + 1) * p.K / G);
@@ -642,21 +677,27 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           // loads of one partial tile are in flight together.  Summation order
           // per element is c_first..c_last (deterministic).
           const int n2 = nt * kTileN + etid;
-          for (int m0 = 0; m0 < rows; m0 += 16) {
-            float acc[16];
+          // CTA c > c_first begins inside this tile (its slot 0); c_first
+          // holds it in slot 1 unless its range starts exactly at the tile.
+          const int cb_first = (int)((int64_t)c_first * p.units / G);
+          const size_t tile_elems = (size_t)BM * kTileN;
+          const float* p_first = p.partials + ((size_t)c_first * 2 + (cb_first >= a ? 0 : 1)) * tile_elems + etid;
+          const float* p_rest = p.partials + etid;  // + (2 c) * tile_elems
+          for (int m0 = 0; m0 < rows; m0 += 8) {
+            float acc[8];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[i] = 0.0f;
-            for (int c = c_first; c <= c_last; ++c) {
-              const int cb = (int)((int64_t)c * p.units / G);  // u_begin of CTA c
-              const float* pt = p.partials + ((size_t)c * 2 + (cb >= a ? 0 : 1)) * (size_t)BM * kTileN +
-                                (size_t)m0 * kTileN + etid;
+            for (int i = 0; i < 8; ++i)
+              acc[i] = (m0 + i < rows) ? __ldcg(p_first + (size_t)(m0 + i) * kTileN) : 0.0f;
+#pragma unroll 4
+            for (int c = c_first + 1; c <= c_last; ++c) {
+              const float* pt = p_rest + (size_t)c * 2 * tile_elems + (size_t)m0 * kTileN;
 #pragma unroll
-              for (int i = 0; i < 16; ++i)
+              for (int i = 0; i < 8; ++i)
                 if (m0 + i < rows) acc[i] += __ldcg(pt + (size_t)i * kTileN);
             }
             if (n2 < p.N) {
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
+              for (int i = 0; i < 8; ++i) {
                 if (m0 + i >= rows) break;
                 const size_t o = (size_t)(mc * BM + m0 + i) * p.ldy + n2;
                 if (p.y_dtype == kF32) static_cast<float*>(p.y)[o] = acc[i];
@@ -820,6 +861,7 @@ static int max_stages(int bm, int ra) {
   int s = 8;
   if (s > tmem_stages) s = tmem_stages;
   while (s > 1 && smem_plan(bm, s, ra).total > kSmemMax) --s;
+  if (s > 4) s &= ~3;  // a multiple of the decoder group count
   return s;
 }
 
@@ -851,19 +893,23 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   return SALR_OK;
 }
 
-static int dec_groups() {
+// Decoder groups: 4 by default (SALR_DEC_GROUPS overrides for experiments),
+// reduced to a divisor of the ring depth (stage ownership, see the kernel).
+static int dec_groups(int stages) {
   static int g = 0;
   if (!g) {
     const char* e = getenv("SALR_DEC_GROUPS");
     g = e ? atoi(e) : 4;
     if (g != 1 && g != 2 && g != 4) g = 4;
   }
-  return g;
+  int ng = g;
+  while (ng > 1 && stages % ng) ng >>= 1;
+  return ng;
 }
 
 template <int BM>
 static int launch_linear(const CUtensorMap* maps, const LinearParams& p, int ctas, cudaStream_t s, bool pdl) {
-  switch (dec_groups()) {
+  switch (dec_groups(p.stages)) {
     case 1: return launch_linear_g<BM, 1>(maps, p, ctas, s, pdl);
     case 2: return launch_linear_g<BM, 2>(maps, p, ctas, s, pdl);
     default: return launch_linear_g<BM, 4>(maps, p, ctas, s, pdl);
@@ -932,7 +978,7 @@ size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pa
 int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const uint8_t* records,
                         const uint32_t* tile_off, int64_t N, const void* acat, const void* bcat_t, int64_t r_pad,
                         void* y, int y_dtype, int64_t ldy, void* workspace, size_t workspace_bytes, int stages,
-                        int num_ctas, void* stream) {
+                        int num_ctas, int flags, void* stream) {
   SALR_CHECK_ARG(M >= 1 && K >= 1 && N >= 1, SALR_ERR_SHAPE, "invalid dims M=%lld K=%lld N=%lld", (long long)M,
                  (long long)K, (long long)N);
   SALR_CHECK_ARG(ldx >= K && ldx % 8 == 0, SALR_ERR_SHAPE, "ldx=%lld must be >= K and a multiple of 8",
@@ -1000,7 +1046,11 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     maps[1] = maps[2] = maps[3] = maps[0];
   }
 
-  int64_t ctas = num_ctas > 0 ? num_ctas : sm_count();
+  // Default grid: one persistent CTA per SM, but at least kMinUnitsPerCta
+  // units each -- small linears (k/v: 512 units) otherwise pay a deep split-K
+  // fixup for a pipeline that never fills.
+  constexpr int64_t kMinUnitsPerCta = 6;
+  int64_t ctas = num_ctas > 0 ? num_ctas : std::min<int64_t>(sm_count(), (p.units + kMinUnitsPerCta - 1) / kMinUnitsPerCta);
   if (ctas > p.units) ctas = p.units;
   SALR_CHECK_ARG(ctas <= 65535, SALR_ERR_CONFIG, "num_ctas too large");
   // in-kernel U needs every CTA resident at once (they wait on each other's
@@ -1012,7 +1062,7 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   p.ldx = (int)ldx;
   p.u_acc = reinterpret_cast<unsigned long long*>(ws + kUAccOff);
   p.ctrl = reinterpret_cast<uint32_t*>(ws + kCtrlOff);
-  bool pdl = false;
+  bool pdl = (flags & SALR_FLAG_PDL) != 0;
   if (p.u_mode == 2) {
     adapter_u_kernel<<<dim3((unsigned)wl.mblocks, (unsigned)wl.ksplit, (unsigned)ra), dim3(64, 4), 0, s>>>(
         static_cast<const __nv_bfloat16*>(x), M, K, ldx, static_cast<const __nv_bfloat16*>(acat), (int)r_pad,

@@ -120,18 +120,27 @@ def validate_transitions(probe: PipelineProbe, capacity: int) -> None:
 # kernel launch
 
 _WS: dict = {}
+_WS_TURN: dict = {}
 
 
 def _workspace(M: int, N: int, K: int, r_pad: int, num_ctas: int, device) -> torch.Tensor:
     """Per-device scratch (grown on demand, zeroed at allocation; the kernels
-    leave its ticket counters zero).  Calls sharing it must be stream-ordered:
-    pass ``workspace=`` to ``salr_linear`` for concurrent streams."""
+    leave its counters in a reusable state).  Two workspaces alternate from
+    call to call, so a launch that overlaps the tail of the previous one
+    (programmatic dependent launch) never shares scratch with it.  Calls on
+    one device must be stream-ordered: pass ``workspace=`` for concurrent
+    streams."""
     need = int(_lib.load().salr_linear_workspace_bytes(M, N, K, r_pad, num_ctas))
-    key = device.index
-    ws = _WS.get(key)
+    turn = _WS_TURN.get(device.index, 0)
+    _WS_TURN[device.index] = turn ^ 1
+    ws = _WS.get((device.index, turn))
     if ws is None or ws.numel() < need:
-        ws = torch.zeros(max(need, 1 << 21), dtype=torch.uint8, device=device)
-        _WS[key] = ws
+        # grow both buffers together (the caching allocator keeps the old ones
+        # alive until the work queued on them is done)
+        size = max(need, 1 << 21)
+        for t in (0, 1):
+            _WS[(device.index, t)] = torch.zeros(size, dtype=torch.uint8, device=device)
+        ws = _WS[(device.index, turn)]
     return ws
 
 
@@ -148,11 +157,14 @@ def _prep_x(x, K: int, check_finite: bool) -> torch.Tensor:
 
 def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *, out: torch.Tensor | None = None,
                 out_dtype: torch.dtype = torch.float32, stages: int = 0, num_ctas: int = 0,
-                check_finite: bool = True, workspace: torch.Tensor | None = None) -> torch.Tensor:
+                check_finite: bool = True, workspace: torch.Tensor | None = None, pdl: bool = False) -> torch.Tensor:
     """Launch the fused B200 kernel: ``x @ decode(s) [+ (x @ a_cat) @ b_cat]``.
 
     ``x`` is rounded to bf16 (the compute format); ``s`` is used with bf16
     values (converted once and cached if it holds float32 values).
+    ``pdl=True`` launches as a programmatic dependent of the preceding kernel
+    (weight streaming overlaps its tail); only valid when that kernel does not
+    read ``out`` and the default alternating workspaces are used.
     """
     _lib.require_cuda()
     if not isinstance(s, BitmapSparseMatrix):
@@ -182,7 +194,7 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     _lib.check(_lib.load().salr_linear_forward(
         _lib.ptr(xb), M, s.rows, int(xb.shape[1]), _lib.ptr(sb.records), _lib.ptr(sb.tile_off), N,
         _lib.ptr(acat), _lib.ptr(bct), r_pad, _lib.ptr(out), _lib.dtype_code(out.dtype), N,
-        _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), _lib.stream_ptr()))
+        _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), 1 if pdl else 0, _lib.stream_ptr()))
     return out
 
 

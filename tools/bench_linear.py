@@ -26,6 +26,7 @@ ap.add_argument("--no-adapters", action="store_true")
 ap.add_argument("--ctas", type=int, default=0)
 ap.add_argument("--stages", type=int, default=0)
 ap.add_argument("--cublas", action="store_true")
+ap.add_argument("--pdl", action="store_true", help="launch as in the stack (programmatic dependent launch)")
 a = ap.parse_args()
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 try:
@@ -72,9 +73,10 @@ for name in a.shapes.split(","):
         del w
     for M in [int(t) for t in a.tokens.split(",")]:
         x = torch.randn(M, K, device="cuda").bfloat16()
-        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-        us = graph_time(lambda i: S.salr_linear(x, mats[i % a.copies], fus[i % a.copies], out=out,
-                                                check_finite=False, num_ctas=a.ctas, stages=a.stages), a.reps)
+        outs = [torch.empty(M, N, device="cuda", dtype=torch.bfloat16) for _ in range(2)]
+        us = graph_time(lambda i: S.salr_linear(x, mats[i % a.copies], fus[i % a.copies], out=outs[i & 1],
+                                                check_finite=False, num_ctas=a.ctas, stages=a.stages,
+                                                pdl=a.pdl), a.reps)
         cb = mats[0].compressed_bytes
         row = {"linear": name, "M": M, "us": round(us, 2), "GBs": round(cb / us / 1e3, 1),
                "frac": round(cb / us / 1e3 / peak, 3)}
