@@ -487,29 +487,86 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       pdl_wait();  // X may be the preceding kernel's output
       par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
       unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
-      const int k0 = (int)((int64_t)blockIdx.x * p.K / G), k1 = (int)((int64_t)(blockIdx.x + 1) * p.K / G);
+      // K slices on 8-element boundaries (16-byte rows for the staged loads)
+      const int k8 = (p.K % 8 == 0) ? 8 : 1, kq = p.K / k8;
+      const int k0 = k8 * (int)((int64_t)blockIdx.x * kq / G), k1 = k8 * (int)((int64_t)(blockIdx.x + 1) * kq / G);
+      // Stage the K slice of A_cat (ks x rp bf16) and row chunks of X
+      // (MCH x ks bf16) in the (still unused) adapter slot with coalesced
+      // 16-byte loads, so the FMA loop runs from shared memory instead of
+      // paying a global-load latency per k.
+      const int ks = k1 - k0;
+      const uint32_t slot_bytes = (uint32_t)p.ra * (kAdTileBytes + 2u * BM * 128u);
+      const uint32_t a_bytes = ((uint32_t)ks * rp * 2u + 15u) & ~15u;
+      const int mch = BM;  // rows per X chunk
+      const bool staged = ks > 0 && (p.K % 8 == 0) && (k0 % 8 == 0) && (ks % 8 == 0) &&
+                          a_bytes + (uint32_t)mch * ks * 2u <= slot_bytes;
       const int mh = etid >> 6;
-      for (int a = 0; a < p.ra; ++a) {
-        const int r = 64 * a + (etid & 63);
-        for (int mb = mh; mb < p.M; mb += 16) {
-          float acc[8];
+      if (staged) {
+        __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(adbuf);
+        __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(adbuf + a_bytes);
+        {  // A slice rows k0..k1 are contiguous in A_cat
+          const uint4* src = reinterpret_cast<const uint4*>(p.acat + (size_t)k0 * rp);
+          uint4* dst = reinterpret_cast<uint4*>(sa);
+          for (int i = etid; i < ks * rp / 8; i += 128) dst[i] = __ldg(src + i);
+        }
+        for (int m0 = 0; m0 < p.M; m0 += mch) {
+          const int rows = min(mch, p.M - m0);
+          named_bar_sync(1, 128);  // previous chunk consumed
+          for (int i = etid; i < rows * (ks / 8); i += 128) {
+            const int m = i / (ks / 8), c = i % (ks / 8);
+            reinterpret_cast<uint4*>(sx + (size_t)m * ks)[c] =
+                __ldg(reinterpret_cast<const uint4*>(p.x + (size_t)(m0 + m) * p.ldx + k0) + c);
+          }
+          named_bar_sync(1, 128);
+          for (int a = 0; a < p.ra; ++a) {
+            const int r = 64 * a + (etid & 63);
+            for (int mb = mh; mb < rows; mb += 16) {
+              float acc[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+              for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
 #pragma unroll 4
-          for (int k = k0; k < k1; ++k) {
-            const float av = __bfloat162float(p.acat[(size_t)k * rp + r]);
+              for (int k = 0; k < ks; ++k) {
+                const float av = __bfloat162float(sa[k * rp + r]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const int m = mb + 2 * i;
+                  if (m < rows) acc[i] = fmaf(__bfloat162float(sx[m * ks + k]), av, acc[i]);
+                }
+              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int m = mb + 2 * i;
+                if (m < rows)
+                  atomicAdd(uacc + (size_t)(m0 + m) * rp + r,
+                            (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
+              }
+            }
+          }
+        }
+        named_bar_sync(1, 128);  // slot free again for the adapter operands
+      } else {
+        for (int a = 0; a < p.ra; ++a) {
+          const int r = 64 * a + (etid & 63);
+          for (int mb = mh; mb < p.M; mb += 16) {
+            float acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll 4
+            for (int k = k0; k < k1; ++k) {
+              const float av = __bfloat162float(p.acat[(size_t)k * rp + r]);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int m = mb + 2 * i;
+                if (m < p.M) acc[i] = fmaf(__bfloat162float(p.x[(size_t)m * p.ldx + k]), av, acc[i]);
+              }
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int m = mb + 2 * i;
-              if (m < p.M) acc[i] = fmaf(__bfloat162float(p.x[(size_t)m * p.ldx + k]), av, acc[i]);
+              if (m < p.M && k1 > k0)
+                atomicAdd(uacc + (size_t)m * rp + r,
+                          (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
             }
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int m = mb + 2 * i;
-            if (m < p.M && k1 > k0)
-              atomicAdd(uacc + (size_t)m * rp + r,
-                        (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
           }
         }
       }
