@@ -139,21 +139,38 @@ def dist_setup(args):
 
 def shard_cols(n: int, world: int, rank: int):
     """128-column-aligned stripe of an output dimension."""
-    tiles = (n + 127) // 128
-    t0 = tiles * rank // world
-    t1 = tiles * (rank + 1) // world
-    return min(128 * t0, n), min(128 * t1, n)
+    from paper_2601_16991_b200.sharding import shard_cols as _sc
+    return _sc(n, world, rank)
 
 
 # ---------------------------------------------------------------------------
 # reference arm: oracle (CPU) on a bounded sample
 
-def cpu_sample(tokens: int, sparsity: float, budget_s: float = 20.0):
-    """Time the oracle port of the reference pipelined_forward (f64, the
-    reference's 64x8-byte tile order) on one layer's 7 linears."""
+def _reference_pkg():
+    """The unmodified reference package installed offline into baseline/_ref
+    (pure Python/NumPy), or None."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "salr")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import salr  # noqa: F401
+        from salr import bitmap, fusion, pipeline, residual
+        return bitmap, fusion, pipeline, residual
+    except Exception:
+        return None
+
+
+def cpu_sample(tokens: int, sparsity: float, budget_s: float = 20.0, prefer_reference: bool = True):
+    """Time the reference CPU path of one layer's 7 linears at M=tokens (a
+    bounded sample of the stack workload; x32 layers extrapolated).
+
+    Prefers the real reference package (``salr.pipeline.pipelined_forward``
+    with its stock ``PipelineConfig()``, from baseline/_ref, kind
+    "reference"); falls back to the oracle port (oracle/salr_oracle.py, kind
+    "port") when baseline/_ref is absent."""
     import numpy as np
-    import torch
-    from oracle import salr_oracle as O
     from paper_2601_16991_b200 import synthetic
 
     try:
@@ -161,39 +178,64 @@ def cpu_sample(tokens: int, sparsity: float, budget_s: float = 20.0):
         blas_threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
     except Exception:
         blas_threads = os.cpu_count()
+    ref = _reference_pkg() if prefer_reference else None
     rng = np.random.default_rng(0)
     x = synthetic.gen_x(tokens, 14336, seed=7).double().numpy()
+    q = {0.3: 0.3853204664075676, 0.5: 0.6744897501960817, 0.7: 1.0364333894937898}[sparsity]
     linears = {}
     for i, name in enumerate(LINEARS):
         k, n = SHAPES[name]
         w = synthetic.gen_weight(k, n, 1000 + i).double().numpy()
-        thr = 0.02 * 0.6744897501960817  # |w| quantile for N(0, 0.02^2) at 50%
-        w[np.abs(w) < thr * (sparsity / 0.5 if sparsity != 0.5 else 1.0)] = 0.0
-        s = O.encode(w)
-        ads = [O.Adapter(rng.normal(size=(k, 16)) / 64, rng.normal(size=(16, n)) * 0.02, 16),
-               O.Adapter(rng.normal(size=(k, 16)) / 64, rng.normal(size=(16, n)) * 0.02, 16, 2.0)]
-        linears[name] = (s, O.fuse(ads), k)
+        w[np.abs(w) < 0.02 * q] = 0.0  # magnitude prune at the N(0, 0.02^2) quantile
+        a = [rng.normal(size=(k, 16)) / 64, rng.normal(size=(k, 16)) / 64]
+        b = [rng.normal(size=(16, n)) * 0.02, rng.normal(size=(16, n)) * 0.02]
+        if ref is not None:
+            bitmap, fusion, pipeline, residual = ref
+            s = bitmap.encode(w)
+            ads = [residual.AdapterPair(a[0], b[0], 16), residual.AdapterPair(a[1], b[1], 16, 2.0)]
+            linears[name] = (s, fusion.fuse(ads), k)
+        else:
+            from oracle import salr_oracle as O
+            s = O.encode(w)
+            ads = [O.Adapter(a[0], b[0], 16), O.Adapter(a[1], b[1], 16, 2.0)]
+            linears[name] = (s, O.fuse(ads), k)
     times = []
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
         for name in LINEARS:
             s, f, k = linears[name]
-            O.pipelined_forward(x[:, :k], s, f)
+            if ref is not None:
+                ref[2].pipelined_forward(x[:, :k], s, f, ref[2].PipelineConfig())
+            else:
+                from oracle import salr_oracle as O
+                O.pipelined_forward(x[:, :k], s, f)
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_start > budget_s or len(times) >= 3:
             break
     layer_s = statistics.median(times)
     step_s = layer_s * 32
-    comp = sum(linears[nm][0].rows * linears[nm][0].bytes_per_row + 4 * linears[nm][0].nnz for nm in LINEARS)
+    comp = sum(linears[nm][0].rows * ((linears[nm][0].cols + 7) // 8) + 4 * linears[nm][0].nnz for nm in LINEARS)
+    what = ("reference salr.pipeline.pipelined_forward (stock PipelineConfig(): 64x8-byte tiles, decoder "
+            "thread + ring, f64) from baseline/_ref" if ref is not None else
+            "oracle port of pipelined_forward (f64, 64x8-byte tiles, serial)")
     return {
-        "value": tokens / step_s, "unit": "tokens/s", "cores": blas_threads, "kind": "port",
-        "sample": f"oracle pipelined_forward (f64, 64x8-byte tiles, serial) over one layer's 7 linears at "
-                  f"M={tokens}, median of {len(times)} passes = {layer_s:.3f} s/layer, x32 layers extrapolated; "
-                  f"{os.cpu_count()} host cores visible, OpenBLAS threads={blas_threads}",
+        "value": tokens / step_s, "unit": "tokens/s", "cores": blas_threads,
+        "kind": "reference" if ref is not None else "port",
+        "sample": f"{what} over one layer's 7 linears at M={tokens}, median of {len(times)} passes = "
+                  f"{layer_s:.3f} s/layer, x32 layers extrapolated; {os.cpu_count()} host cores visible, "
+                  f"OpenBLAS threads={blas_threads}",
         "compressed_gbs": comp * 32 / step_s / 1e9,
         "layer_s": layer_s,
     }
+
+
+def stack_config(args, world, how):
+    return {"workload": "llama3-8b 32-layer SALR linear stack (q,k,v,o,gate,up,down; configs[1] shapes x32 "
+                        "layers = configs[3] at this N), one decode token-batch per step",
+            "tokens": args.tokens, "layers": 32, "sparsity": args.sparsity, "adapters": "r16+r16 fused (R=32)",
+            "parallelism": f"col-shard{world}" if world > 1 else "single",
+            "l2": "working set 7.85 GB >> 126 MB L2 (inputs larger than L2)", "execution": how}
 
 
 def run_reference(args):
@@ -210,8 +252,7 @@ def run_reference(args):
         "metric": METRIC, "impl": "reference", "value": res["value"], "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "llama3-8b 32-layer SALR linear stack, decode batch", "tokens": args.tokens,
-                   "layers": 32, "sparsity": args.sparsity, "adapters": "r16+r16"},
+        "config": stack_config(args, world, "CPU (reference host path)"),
         "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "compressed_gbs": res["compressed_gbs"],
@@ -274,17 +315,10 @@ class StackRunner:
 
     def _gather(self, locals_, widths):
         """All-gather column shards of one or more linears into full rows."""
-        import torch
-        import torch.distributed as dist
         if self.world == 1:
             return locals_
-        out = []
-        for t, w in zip(locals_, widths):
-            g = torch.empty(self.world, *t.shape, dtype=t.dtype, device=t.device)
-            dist.all_gather_into_tensor(g, t.contiguous(), group=self.group)
-            # rank-major shards -> full columns (shards are 128-col stripes in rank order)
-            out.append(g.permute(1, 0, 2).reshape(t.shape[0], -1)[:, :w])
-        return out
+        from paper_2601_16991_b200.sharding import gather_columns
+        return [gather_columns(t, w, group=self.group) for t, w in zip(locals_, widths)]
 
     def step(self, x):
         S = self.S
@@ -530,12 +564,7 @@ def run_salr(args):
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic random-init weights/inputs",
-            "config": {"workload": "llama3-8b 32-layer SALR linear stack (q,k,v,o,gate,up,down; configs[1] "
-                                   "shapes x32 layers = configs[3] at this N), one decode token-batch per step",
-                       "tokens": M, "layers": args.layers, "sparsity": args.sparsity, "adapters": "r16+r16 fused (R=32)",
-                       "parallelism": f"col-shard{world}" if world > 1 else "single",
-                       "l2": "working set 7.85 GB >> 126 MB L2 (inputs larger than L2)",
-                       "graph": "CUDA graph per step" if use_graph else "eager (NCCL all-gathers)"},
+            "config": stack_config(args, world, "CUDA graph per step" if use_graph else "eager (NCCL all-gathers)"),
             "compressed_gbs": comp_bytes / (ms_per_step / 1e3) / 1e9,
             "compressed_bytes_per_step": comp_bytes,
             "roofline": roof,

@@ -58,9 +58,15 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
-// Spin on test_wait: measured on B200, the suspending try_wait loop added
-// ~0.4 us of wake-up latency to every producer/consumer hand-off.
+// Blocking wait: try_wait lets the hardware park the warp until the phase
+// completes (or a time limit), so waiting warps do not burn issue slots that
+// the decoder warps need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  while (!mbar_try_wait(bar, phase)) {
+  }
+}
+// Spinning wait (no suspension) for very short expected waits.
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t phase) {
   while (!mbar_test_wait(bar, phase)) {
   }
 }
