@@ -104,6 +104,8 @@ int salr_from_reference_write(const uint8_t* bitmap, const void* values, int val
 
 /* ---- SALR linear forward (reference pipeline.py:405-461, fusion.py:87-130) */
 /* Y (M x N) = X (M x K) @ decode(W) + (X @ A_cat) @ B_cat.
+ *   max_record_bytes  largest TB record of W (16 * max(tile_off[t+1]-tile_off[t])),
+ *             sizes the shared-memory ring slots; <= 0 means the worst case
  *   x      bf16, row-major, leading dim ldx (ldx % 8 == 0, 16-byte aligned)
  *   acat   bf16 K x r_pad row-major (zero-padded rank columns) or NULL
  *   bcat_t bf16 (n_nt*128) x r_pad row-major = B_cat^T, zero padded, or NULL
@@ -130,7 +132,7 @@ int salr_debug_set_trace(void* buf);
  * a workspace the preceding kernel does not use (alternate two). */
 #define SALR_FLAG_PDL 1
 int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const uint8_t* records,
-                        const uint32_t* tile_off, int64_t N, const void* acat, const void* bcat_t,
+                        const uint32_t* tile_off, int64_t max_record_bytes, int64_t N, const void* acat, const void* bcat_t,
                         int64_t r_pad, void* y, int y_dtype, int64_t ldy, void* workspace,
                         size_t workspace_bytes, int stages, int num_ctas, int flags, void* stream);
 

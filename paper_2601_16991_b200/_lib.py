@@ -38,7 +38,7 @@ _SIGS = {
     "salr_from_reference_write": ([_vp, _vp, _int, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp], _int),
     "salr_linear_workspace_bytes": ([_i64, _i64, _i64, _i64, _int], ctypes.c_size_t),
     "salr_debug_set_trace": ([_vp], _int),
-    "salr_linear_forward": ([_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _i64, _vp, _int, _i64,
+    "salr_linear_forward": ([_vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _int, _i64,
                              _vp, ctypes.c_size_t, _int, _int, _int, _vp], _int),
 }
 EXPORTS = tuple(_SIGS)

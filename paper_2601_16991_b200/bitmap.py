@@ -127,6 +127,8 @@ class BitmapSparseMatrix:
         obj = cls.__new__(cls)
         obj._init_geometry(rows, cols, value_dtype)
         obj.records, obj.tile_off = records, tile_off
+        obj._max_rec = None
+        obj.max_record_bytes  # computed eagerly (never inside a graph capture)
         obj.nnz = obj._count_nnz()
         return obj
 
@@ -156,6 +158,8 @@ class BitmapSparseMatrix:
                                                  self.rows, self.cols, vcode, _u32(rowtile_off), _u32(tile_cnt),
                                                  _u32(tile_off), _lib.ptr(records), s))
         self.records, self.tile_off = records, tile_off
+        self._max_rec = None
+        self.max_record_bytes  # computed eagerly (never inside a graph capture)
         self.nnz = total_nnz
 
     def _to_reference(self):
@@ -208,6 +212,14 @@ class BitmapSparseMatrix:
         return self.rows * self.bytes_per_row + _VALUE_DTYPES[self.value_dtype][2] * self.nnz
 
     @property
+    def max_record_bytes(self) -> int:
+        """Largest TB record (bytes); sizes the linear kernel's ring slots."""
+        if getattr(self, "_max_rec", None) is None:
+            off = self.tile_off.to(torch.int64) & 0xFFFFFFFF
+            self._max_rec = int(16 * (off[1:] - off[:-1]).max().item()) if off.numel() > 1 else 0
+        return self._max_rec
+
+    @property
     def device_bytes(self) -> int:
         """Actual TB bytes resident in HBM (records incl. headers/padding + offsets)."""
         return int(self.records.numel()) + 4 * int(self.tile_off.numel())
@@ -252,6 +264,8 @@ def encode(m, value_dtype: str = "f32") -> BitmapSparseMatrix:
     _lib.check(lib.salr_encode_write(_lib.ptr(dense), icode, rows, cols, cols, vcode, _u32(tile_cnt),
                                      _u32(tile_off), _lib.ptr(records), st))
     s.records, s.tile_off = records, tile_off
+    s._max_rec = None
+    s.max_record_bytes  # computed eagerly (never inside a graph capture)
     s.nnz = int(tile_cnt.sum().item())
     return s
 

@@ -192,7 +192,8 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     else:
         ws = workspace
     _lib.check(_lib.load().salr_linear_forward(
-        _lib.ptr(xb), M, s.rows, int(xb.shape[1]), _lib.ptr(sb.records), _lib.ptr(sb.tile_off), N,
+        _lib.ptr(xb), M, s.rows, int(xb.shape[1]), _lib.ptr(sb.records), _lib.ptr(sb.tile_off),
+        sb.max_record_bytes, N,
         _lib.ptr(acat), _lib.ptr(bct), r_pad, _lib.ptr(out), _lib.dtype_code(out.dtype), N,
         _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), 1 if pdl else 0, _lib.stream_ptr()))
     return out

@@ -42,7 +42,7 @@ def test_argument_validation_without_device():
     rc = lib.salr_decode(None, None, 0, 4, 8, 0, 5, 0, 8, None, 0, 8, None)
     assert rc == 3
     # r_pad other than 0/64/128 -> ConfigError
-    rc = lib.salr_linear_forward(None, 1, 64, 64, None, None, 128, None, None, 32, None, 0, 128, None, 0, 0, 0, 0, None)
+    rc = lib.salr_linear_forward(None, 1, 64, 64, None, None, 0, 128, None, None, 32, None, 0, 128, None, 0, 0, 0, 0, None)
     assert rc in (1, 4)
 
 
