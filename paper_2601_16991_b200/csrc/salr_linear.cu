@@ -86,7 +86,7 @@ constexpr int kUFrac = 26;
 constexpr int kCtrlEpoch = 0, kCtrlDone = 1, kCtrlReady = 2, kCtrlUsed = 4;
 constexpr int kUAccElems = 256 * 128;  // per parity buffer: M <= 256 rows x r_pad <= 128
 constexpr int kNumDecWarps = 16;
-constexpr int kNumThreads = 800;               // 25 warps
+constexpr int kNumThreads = 896;               // 28 warps
 constexpr int kFirstDecWarp = 4;
 constexpr int kFirstEpiWarp = 20;
 constexpr uint32_t kAdTileBytes = 128 * 128;   // B_cat^T tile: 128 rows x 64 bf16
@@ -146,6 +146,7 @@ __device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t 
 // kDecGroups decoder groups (group g decodes units it = g mod kDecGroups).
 constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPrep0 = 2, kWarpPrep1 = 3;
 constexpr int kWarpProd1 = 24;
+constexpr int kWarpPrep2 = 25, kWarpPrep3 = 26;  // warp 27 idle
 
 template <int BM, int kDecGroups>
 __global__ void __launch_bounds__(kNumThreads, 1)
@@ -311,6 +312,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // uniform state stays in uniform registers); one elected lane issues.
     int s = 0, seg = 0;
     uint32_t ph = 0, ad_ph = 0;
+    bool ready = false;
     int u = u_begin;
     while (u < u_end) {
       const int tile_base = u - u % p.n_kt;
@@ -321,8 +323,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       mbar_wait(&acc_empty[b], acc_ph ^ 1);
       tc_fence_after();
       for (int v = u; v < seg_end; ++v) {
-        mbar_wait(&decoded[s], ph);
+        if (!ready) mbar_wait(&decoded[s], ph);
         tc_fence_after();
+        // Probe the next unit's barrier now: the ~150-cycle round trip of the
+        // probe overlaps this unit's MMA issue instead of serialising with it.
+        int s2 = s + 1;
+        uint32_t ph2 = ph;
+        if (s2 == S) { s2 = 0; ph2 ^= 1; }
+        const bool next_ready = (v + 1 < u_end) && mbar_test_wait(&decoded[s2], ph2);
         if (elect_one()) {
           const uint64_t bdesc = desc_kmajor_sw128(smem_u32(xbuf + (size_t)s * BM * 128));
           const uint32_t a_tm = tmem + a_col0 + 32u * s;
@@ -334,7 +342,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           SALR_TRACE_UNIT(5, v - u_begin);
         }
         __syncwarp();
-        if (++s == S) { s = 0; ph ^= 1; }
+        s = s2;
+        ph = ph2;
+        ready = next_ready;
       }
       if (u == tile_base && p.ra) {
         mbar_wait(ad_full, ad_ph);
@@ -363,15 +373,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       ++seg;
       u = seg_end;
     }
-  } else if (warp == kWarpPrep0 || warp == kWarpPrep1) {
+  } else if (warp == kWarpPrep0 || warp == kWarpPrep1 || warp == kWarpPrep2 || warp == kWarpPrep3) {
     // ================= row bases (two warps, alternate units): exclusive
     // prefix of the bitmap row popcounts per 32-column group -> smem table of
     // the shared-memory byte address where each (group, row) value run starts.
     // lane l handles rows 2l, 2l+1 of all four groups.
-    const int w2 = warp - kWarpPrep0;
+    // row-base warps: 4 when the ring depth allows (stage ownership), else 2 / 1
+    const int NR = (S % 4 == 0) ? 4 : NP;
+    const int w2 = warp <= kWarpPrep1 ? warp - kWarpPrep0 : warp - kWarpPrep2 + 2;
     int s = w2;
     uint32_t ph = 0;
-    for (int it = u_begin + w2; it < u_end && (w2 < NP); it += NP) {
+    for (int it = u_begin + w2; it < u_end && (w2 < NR); it += NR) {
       mbar_wait(&full[s], ph);
       if (lane == 0) SALR_TRACE_UNIT(1, it - u_begin);
       const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
@@ -414,7 +426,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         SALR_TRACE(it == u_begin ? 3 : 12);
         SALR_TRACE_UNIT(2, it - u_begin);
       }
-      s += NP;
+      s += NR;
       if (s >= S) { s -= S; ph ^= 1; }
     }
   } else if (warp >= kFirstDecWarp && warp < kFirstEpiWarp) {
