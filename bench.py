@@ -284,6 +284,7 @@ def build_stack(layers, world, rank, sparsity, device):
             w = (torch.randn(k, nl, generator=g, device=device) * 0.02).to(torch.bfloat16)
             w = torch.where(w.float().abs() < thr, torch.zeros_like(w), w)
             s = S.encode(w, value_dtype="bf16")
+            s.compute_format()  # the linear kernel's operand format, built once at load
             del w
             ads = [S.AdapterPair((torch.randn(k, 16, generator=g, device=device) / 64).bfloat16().float(),
                                  (torch.randn(16, nl, generator=g, device=device) * 0.02).bfloat16().float(), 16),

@@ -102,9 +102,20 @@ int salr_from_reference_write(const uint8_t* bitmap, const void* values, int val
                               const uint32_t* rowtile_off, const uint32_t* tile_cnt,
                               const uint32_t* tile_off, uint8_t* records, void* stream);
 
+/* ---- TB2 compute format (linear kernel operand; built once per matrix) --- */
+/* From bf16 TB records: tile_off2[n_tiles + 1] (16-byte units), then the
+ * TB2 records (layout in csrc/salr_format.cuh: per tile the column masks,
+ * band offsets and band-column-major values, so a decoder lane reads its
+ * column's values contiguously).  Same logical bitmap and values. */
+int salr_tb2_count(const uint8_t* records, const uint32_t* tile_off, int64_t rows, int64_t cols,
+                   uint32_t* tile_off2, void* stream);
+int salr_tb2_write(const uint8_t* records, const uint32_t* tile_off, int64_t rows, int64_t cols,
+                   const uint32_t* tile_off2, uint8_t* records2, void* stream);
+
 /* ---- SALR linear forward (reference pipeline.py:405-461, fusion.py:87-130) */
 /* Y (M x N) = X (M x K) @ decode(W) + (X @ A_cat) @ B_cat.
- *   max_record_bytes  largest TB record of W (16 * max(tile_off[t+1]-tile_off[t])),
+ *   records / tile_off  W in the TB2 compute format (salr_tb2_*)
+ *   max_record_bytes  largest TB2 record of W (16 * max(tile_off[t+1]-tile_off[t])),
  *             sizes the shared-memory ring slots; <= 0 means the worst case
  *   x      bf16, row-major, leading dim ldx (ldx % 8 == 0, 16-byte aligned)
  *   acat   bf16 K x r_pad row-major (zero-padded rank columns) or NULL

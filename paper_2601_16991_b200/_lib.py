@@ -36,6 +36,8 @@ _SIGS = {
     "salr_to_reference": ([_vp, _vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _vp], _int),
     "salr_from_reference_count": ([_vp, _i64, _i64, _int, _vp, _vp, _vp, _vp], _int),
     "salr_from_reference_write": ([_vp, _vp, _int, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp], _int),
+    "salr_tb2_count": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
+    "salr_tb2_write": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp], _int),
     "salr_linear_workspace_bytes": ([_i64, _i64, _i64, _i64, _int], ctypes.c_size_t),
     "salr_debug_set_trace": ([_vp], _int),
     "salr_linear_forward": ([_vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _int, _i64,

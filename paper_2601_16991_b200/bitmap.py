@@ -20,7 +20,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import BoundsError, CorruptionError, DomainError, FormatError, ShapeError
+from .errors import BoundsError, CorruptionError, DomainError, FormatError, SalrError, ShapeError
 from .linalg import as_matrix, to_cuda
 from .residual import AdapterPair
 
@@ -223,6 +223,29 @@ class BitmapSparseMatrix:
     def device_bytes(self) -> int:
         """Actual TB bytes resident in HBM (records incl. headers/padding + offsets)."""
         return int(self.records.numel()) + 4 * int(self.tile_off.numel())
+
+    def compute_format(self):
+        """(records2, tile_off2, max_record_bytes) of the TB2 compute format
+        the linear kernel consumes; built once from the bf16 TB records on the
+        current stream and cached (never inside a CUDA-graph capture)."""
+        if getattr(self, "_tb2", None) is None:
+            if torch.cuda.is_current_stream_capturing():
+                raise SalrError("build the compute format (BitmapSparseMatrix.compute_format()) before "
+                                "capturing a CUDA graph")
+            sb = self.to_bf16()
+            lib = _lib.load()
+            st = _lib.stream_ptr()
+            off2 = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=sb.records.device)
+            _lib.check(lib.salr_tb2_count(_lib.ptr(sb.records), _u32(sb.tile_off), self.rows, self.cols,
+                                          _u32(off2), st))
+            units = int(off2[-1].item()) & 0xFFFFFFFF
+            rec2 = torch.empty(16 * units, dtype=torch.uint8, device=sb.records.device)
+            _lib.check(lib.salr_tb2_write(_lib.ptr(sb.records), _u32(sb.tile_off), self.rows, self.cols,
+                                          _u32(off2), _lib.ptr(rec2), st))
+            o = off2.to(torch.int64) & 0xFFFFFFFF
+            mx = int(16 * (o[1:] - o[:-1]).max().item()) if o.numel() > 1 else 0
+            self._tb2 = (rec2, off2, mx)
+        return self._tb2
 
     def to_bf16(self) -> "BitmapSparseMatrix":
         """The same matrix with bf16 values (the linear kernel's operand format)."""

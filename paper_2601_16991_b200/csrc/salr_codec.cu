@@ -374,6 +374,68 @@ static int check_dims(int64_t rows, int64_t cols) {
 
 using namespace salr;
 
+
+// ------------------------------------------------------------------ TB2 (compute format)
+struct Tb2UnitsFn {
+  const uint8_t* records;
+  const uint32_t* tile_off;
+  __device__ uint32_t operator()(int64_t t) const {
+    const uint32_t nnz = reinterpret_cast<const uint32_t*>(records + 16ull * tile_off[t])[3];
+    return (uint32_t)((kT2Val + 2u * nnz + 15u) / 16u);
+  }
+};
+
+// grid = n_tiles, block = 128: thread n <-> tile column n (warp q = column group).
+__global__ void tb2_write_kernel(const uint8_t* __restrict__ records, const uint32_t* __restrict__ tile_off,
+                                 const uint32_t* __restrict__ tile_off2, uint8_t* __restrict__ records2) {
+  const int64_t t = blockIdx.x;
+  const int q = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const uint8_t* src = records + 16ull * tile_off[t];
+  uint8_t* dst = records2 + 16ull * tile_off2[t];
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(src);
+  const uint32_t* bits = hdr + 4 + q * kTileK;
+  const uint32_t goff = q ? hdr[q - 1] : 0u;
+  const uint32_t lt = lanemask_lt();
+  uint64_t m = 0;
+  for (int r = 0; r < kTileK; ++r)
+    if ((bits[r] >> l) & 1u) m |= 1ull << r;
+  uint32_t excl[16], boff[16];
+  uint32_t run = 0;
+  for (int b = 0; b < 16; ++b) {
+    const uint32_t c = (uint32_t)__popcll((m >> (4 * b)) & 0xFull);
+    uint32_t incl = c;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (l >= d) incl += y;
+    }
+    excl[b] = incl - c;
+    boff[b] = run;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(dst)[threadIdx.x] = hdr[threadIdx.x];
+  if (l < 16) reinterpret_cast<uint16_t*>(dst + kT2BandOff)[q * 16 + l] = (uint16_t)boff[l];
+  reinterpret_cast<uint64_t*>(dst + kT2Mask)[threadIdx.x] = m;
+  const uint16_t* sv = reinterpret_cast<const uint16_t*>(src + kValOffset);
+  uint16_t* dv = reinterpret_cast<uint16_t*>(dst + kT2Val);
+  uint32_t rowpref = 0;
+  for (int r = 0; r < kTileK; ++r) {
+    const uint32_t w = bits[r];
+    if ((w >> l) & 1u) {
+      const int b = r >> 2;
+      const uint32_t nib = (uint32_t)((m >> (4 * b)) & 0xFull);
+      const uint32_t rank = __popc(nib & ((1u << (r & 3)) - 1u));
+      dv[goff + boff[b] + excl[b] + rank] = sv[goff + rowpref + __popc(w & lt)];
+    }
+    rowpref += __popc(w);
+  }
+  if (threadIdx.x < 16) {
+    const uint32_t used = kT2Val + 2u * hdr[3];
+    const uint32_t end = 16u * (tile_off2[t + 1] - tile_off2[t]);
+    const uint32_t bpos = used + threadIdx.x;
+    if (bpos < end) dst[bpos] = 0;
+  }
+}
+
 extern "C" {
 
 int salr_version(void) { return 1; }
@@ -508,6 +570,29 @@ int salr_from_reference_write(const uint8_t* bitmap, const void* values, int val
   ref_to_tb_kernel<<<(unsigned)(n_kt * n_nt), 128, 0, static_cast<cudaStream_t>(stream)>>>(
       bitmap, values, values_dtype, rows, cols, n_kt, n_nt, value_dtype, rowtile_off, tile_cnt, tile_off,
       records);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+
+int salr_tb2_count(const uint8_t* records, const uint32_t* tile_off, int64_t rows, int64_t cols,
+                   uint32_t* tile_off2, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  scan1_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(Tb2UnitsFn{records, tile_off}, n_kt * n_nt,
+                                                                  tile_off2);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_tb2_write(const uint8_t* records, const uint32_t* tile_off, int64_t rows, int64_t cols,
+                   const uint32_t* tile_off2, uint8_t* records2, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  tb2_write_kernel<<<(unsigned)(n_kt * n_nt), 128, 0, static_cast<cudaStream_t>(stream)>>>(records, tile_off,
+                                                                                           tile_off2, records2);
   SALR_LAUNCH_CHECK();
   return SALR_OK;
 }

@@ -14,6 +14,20 @@ constexpr int kBitsBytes = kGroups * kTileK * 4;      // 1024
 constexpr int kValOffset = kHdrBytes + kBitsBytes;    // 1040
 constexpr int kMaxRecordBytesBf16 = kValOffset + kTileK * kTileN * 2;  // 17424
 
+// TB2: the linear kernel's compute format, built once per matrix from bf16
+// TB records (salr_tb2_*).  Same tile grid, same logical content; per tile:
+//   u32 hdr[4]           value offsets of groups 1,2,3 and the tile nnz
+//   u16 bandoff[4][16]   per 32-column group g and 4-row band b: offset of the
+//                        band's values from the group's first value
+//   u64 cmask[128]       cmask[n] bit r <=> element (row r, col n) nonzero
+//   bf16 values          group-major; within a group band-major; within a band
+//                        column-major; within a column ascending rows
+// so a decoder lane (one output column) finds its band's values contiguous.
+constexpr int kT2BandOff = 16;
+constexpr int kT2Mask = 144;
+constexpr int kT2Val = 1168;
+constexpr int kMaxRecordBytesT2 = kT2Val + kTileK * kTileN * 2;  // 17552
+
 enum : int { kF32 = 0, kBF16 = 1, kF64 = 2 };
 
 __host__ __device__ inline int value_bytes(int dtype) { return dtype == kF32 ? 4 : 2; }

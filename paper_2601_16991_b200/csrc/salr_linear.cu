@@ -86,7 +86,7 @@ constexpr int kUFrac = 26;
 constexpr int kCtrlEpoch = 0, kCtrlDone = 1, kCtrlReady = 2, kCtrlUsed = 4;
 constexpr int kUAccElems = 256 * 128;  // per parity buffer: M <= 256 rows x r_pad <= 128
 constexpr int kNumDecWarps = 16;
-constexpr int kNumThreads = 896;               // 28 warps
+constexpr int kNumThreads = 800;               // 25 warps
 constexpr int kFirstDecWarp = 4;
 constexpr int kFirstEpiWarp = 20;
 constexpr uint32_t kAdTileBytes = 128 * 128;   // B_cat^T tile: 128 rows x 64 bf16
@@ -106,8 +106,8 @@ __host__ __device__ inline SmemPlan smem_plan(int bm, int stages, int ra, uint32
   p.x_off = p.ad_off + ad_bytes;                           // stages x BM x 128 B
   p.rec_off = p.x_off + (uint32_t)stages * bm * 128u;      // stages x kRecSlot
   p.base_off = p.rec_off + (uint32_t)stages * rec_slot;    // stages x 256 u32
-  p.bar_off = p.base_off + (uint32_t)stages * 1024u;
-  p.total = p.bar_off + 8u * (4u * stages + 6u) + 16u + 1024u;  // + tmem slot + alignment slack
+  p.bar_off = p.base_off;
+  p.total = p.bar_off + 8u * (3u * stages + 6u) + 16u + 1024u;  // + tmem slot + alignment slack
   return p;
 }
 
@@ -144,9 +144,8 @@ __device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t 
 // each serial role is split across warps that work on different units
 // concurrently: two producers (even / odd units), two row-base warps, and
 // kDecGroups decoder groups (group g decodes units it = g mod kDecGroups).
-constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPrep0 = 2, kWarpPrep1 = 3;
+constexpr int kWarpProd0 = 0, kWarpMma = 1;  // warps 2-3 idle
 constexpr int kWarpProd1 = 24;
-constexpr int kWarpPrep2 = 25, kWarpPrep3 = 26;  // warp 27 idle
 
 template <int BM, int kDecGroups>
 __global__ void __launch_bounds__(kNumThreads, 1)
@@ -167,12 +166,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int S = p.stages;
   uint8_t* xbuf = smem + p.x_off;
   uint8_t* recbuf = smem + p.rec_off;
-  uint32_t* basetab = reinterpret_cast<uint32_t*>(smem + p.base_off);
   uint8_t* adbuf = smem + p.ad_off;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   uint64_t* empty = full + S;
-  uint64_t* prepd = empty + S;
-  uint64_t* decoded = prepd + S;
+  uint64_t* decoded = empty + S;
   uint64_t* acc_full = decoded + S;    // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint64_t* ad_full = acc_empty + 2;
@@ -266,7 +263,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       for (int s = 0; s < S; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], 1);
-        mbar_init(&prepd[s], 1);
         mbar_init(&decoded[s], WPG);
       }
       for (int b = 0; b < 2; ++b) {
@@ -373,106 +369,74 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       ++seg;
       u = seg_end;
     }
-  } else if (warp == kWarpPrep0 || warp == kWarpPrep1 || warp == kWarpPrep2 || warp == kWarpPrep3) {
-    // ================= row bases (two warps, alternate units): exclusive
-    // prefix of the bitmap row popcounts per 32-column group -> smem table of
-    // the shared-memory byte address where each (group, row) value run starts.
-    // lane l handles rows 2l, 2l+1 of all four groups.
-    // row-base warps: 4 when the ring depth allows (stage ownership), else 2 / 1
-    const int NR = (S % 4 == 0) ? 4 : NP;
-    const int w2 = warp <= kWarpPrep1 ? warp - kWarpPrep0 : warp - kWarpPrep2 + 2;
-    int s = w2;
-    uint32_t ph = 0;
-    for (int it = u_begin + w2; it < u_end && (w2 < NR); it += NR) {
-      mbar_wait(&full[s], ph);
-      if (lane == 0) SALR_TRACE_UNIT(1, it - u_begin);
-      const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
-      const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec);
-      const uint32_t* bits = hdr + 4;
-      uint32_t ca[4], cb[4];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const uint2 wv = *reinterpret_cast<const uint2*>(bits + g * kTileK + 2 * lane);
-        ca[g] = __popc(wv.x);
-        cb[g] = __popc(wv.y);
-      }
-      // two 16-bit lanes per register: counts per lane <= 64, prefixes <= 4096
-      uint32_t p01 = (ca[0] + cb[0]) | ((ca[1] + cb[1]) << 16);
-      uint32_t p23 = (ca[2] + cb[2]) | ((ca[3] + cb[3]) << 16);
-      const uint32_t own01 = p01, own23 = p23;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t t01 = __shfl_up_sync(0xffffffffu, p01, d);
-        const uint32_t t23 = __shfl_up_sync(0xffffffffu, p23, d);
-        if ((int)lane >= d) {
-          p01 += t01;
-          p23 += t23;
-        }
-      }
-      p01 -= own01;
-      p23 -= own23;
-      const uint32_t vbase = smem_u32(rec) + kValOffset;
-      const uint32_t goff[4] = {0u, hdr[0], hdr[1], hdr[2]};
-      const uint32_t ex[4] = {p01 & 0xffffu, p01 >> 16, p23 & 0xffffu, p23 >> 16};
-      uint32_t* tab = basetab + (size_t)s * 256;
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        const uint32_t b0 = vbase + 2u * (goff[g] + ex[g]);
-        *reinterpret_cast<uint2*>(tab + g * kTileK + 2 * lane) = make_uint2(b0, b0 + 2u * ca[g]);
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&prepd[s]);
-        SALR_TRACE(it == u_begin ? 3 : 12);
-        SALR_TRACE_UNIT(2, it - u_begin);
-      }
-      s += NR;
-      if (s >= S) { s -= S; ph ^= 1; }
-    }
   } else if (warp >= kFirstDecWarp && warp < kFirstEpiWarp) {
-    // ================= decoders.  Group g = units it = g (mod kDecGroups);
-    // warp (g, part, q) owns TMEM lanes 32q..32q+31 (output columns of group
-    // q) and rows part*RPW .. part*RPW + RPW - 1 of the tile.
+    // ================= decoders (TB2 records).  Group g = units it = g (mod
+    // kDecGroups); warp (g, part, q) owns TMEM lanes 32q..32q+31 (output
+    // columns of group q) and bands part*BPW .. of the tile.  Per lane (one
+    // output column) and 4-row band the values are contiguous: the band's
+    // run start is bandoff[q][b] + (exclusive warp prefix of the band
+    // counts), and a predicated pointer chain expands the 4 rows -- no
+    // per-element rank popcounts.
+    constexpr int BPW = RPW / 4;  // bands per decoder warp
     const int dw = warp - kFirstDecWarp;
     const int grp = dw / WPG;
     const int part = (dw % WPG) >> 2;
     const int q = warp & 3;
-    const uint32_t lt = lanemask_lt();
-    const uint32_t lanebit = 1u << lane;
     const uint32_t lane_tm = (uint32_t)(32 * q) << 16;
-    const uint32_t raw_u32 = smem_u32(smem_raw);
     int s = grp;  // S is a multiple of kDecGroups (host)
     uint32_t ph = 0;
     for (int it = u_begin + grp; it < u_end; it += kDecGroups) {
       mbar_wait(&full[s], ph);
-      mbar_wait(&prepd[s], ph);
-      const uint32_t* bits =
-          reinterpret_cast<const uint32_t*>(recbuf + (size_t)s * p.rec_slot) + 4 + q * kTileK + RPW * part;
-      const uint32_t* tab = basetab + (size_t)s * 256 + q * kTileK + RPW * part;
-      const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(RPW / 2 * part);
+      const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
+      const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(2 * BPW * part);
       if (!(p.dbg & 1)) {
+        const uint2 mw = *reinterpret_cast<const uint2*>(rec + kT2Mask + 8 * (32 * q + lane));
+        const uint32_t goff = q ? reinterpret_cast<const uint32_t*>(rec)[q - 1] : 0u;
+        const uint4 bo0 = *reinterpret_cast<const uint4*>(rec + kT2BandOff + 32 * q);
+        const uint4 bo1 = *reinterpret_cast<const uint4*>(rec + kT2BandOff + 32 * q + 16);
+        const uint32_t bo[8] = {bo0.x, bo0.y, bo0.z, bo0.w, bo1.x, bo1.y, bo1.z, bo1.w};
+        // band counts (4-bit fields) -> bytes: c[0] bands 0,2,4,6; c[1] 1,3,5,7;
+        // c[2] 8,10,12,14; c[3] 9,11,13,15
+        uint32_t nl = mw.x - ((mw.x >> 1) & 0x55555555u);
+        nl = (nl & 0x33333333u) + ((nl >> 2) & 0x33333333u);
+        uint32_t nh = mw.y - ((mw.y >> 1) & 0x55555555u);
+        nh = (nh & 0x33333333u) + ((nh >> 2) & 0x33333333u);
+        const uint32_t c[4] = {nl & 0x0F0F0F0Fu, (nl >> 4) & 0x0F0F0F0Fu, nh & 0x0F0F0F0Fu, (nh >> 4) & 0x0F0F0F0Fu};
+        uint32_t e[4] = {c[0], c[1], c[2], c[3]};
 #pragma unroll
-        for (int c = 0; c < RPW / 16; ++c) {  // 16-row chunks -> 8 TMEM columns
-          uint32_t w[16], bs[16];
+        for (int d = 1; d < 32; d <<= 1) {  // inclusive scan, byte lanes (<= 128)
+          uint32_t t[4];
 #pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            const uint4 wv = *reinterpret_cast<const uint4*>(bits + 16 * c + i);
-            const uint4 bv = *reinterpret_cast<const uint4*>(tab + 16 * c + i);
-            w[i] = wv.x; w[i + 1] = wv.y; w[i + 2] = wv.z; w[i + 3] = wv.w;
-            bs[i] = bv.x; bs[i + 1] = bv.y; bs[i + 2] = bv.z; bs[i + 3] = bv.w;
+          for (int j = 0; j < 4; ++j) t[j] = __shfl_up_sync(0xffffffffu, e[j], d);
+          if ((int)lane >= d) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) e[j] += t[j];
           }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) e[j] -= c[j];
+        const uint32_t vbase = (uint32_t)(rec - smem_raw) + kT2Val + 2u * goff;
+#pragma unroll
+        for (int c4 = 0; c4 < BPW / 4; ++c4) {  // 4 bands -> 8 TMEM columns
           uint32_t packed[8];
 #pragma unroll
-          for (int i = 0; i < 16; i += 2) {
-            uint32_t v0 = 0u, v1 = 0u;
-            if (w[i] & lanebit)
-              v0 = *reinterpret_cast<const uint16_t*>(smem_raw + (bs[i] - raw_u32 + 2u * __popc(w[i] & lt)));
-            if (w[i + 1] & lanebit)
-              v1 = *reinterpret_cast<const uint16_t*>(smem_raw +
-                                                      (bs[i + 1] - raw_u32 + 2u * __popc(w[i + 1] & lt)));
-            packed[i >> 1] = __byte_perm(v0, v1, 0x5410);
+          for (int i = 0; i < 4; ++i) {
+            const int b = BPW * part + 4 * c4 + i;  // compile-time when part == 0
+            const uint32_t ev = e[(b >= 8 ? 2 : 0) + (b & 1)];
+            const uint32_t ex = (ev >> (8 * ((b & 7) >> 1))) & 0xFFu;
+            const uint32_t bov = (bo[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
+            uint32_t r = vbase + 2u * (bov + ex);
+            const uint32_t word = b < 8 ? mw.x : mw.y;
+            const int sh = 4 * (b & 7);
+            uint32_t v0 = 0u, v1 = 0u, v2 = 0u, v3 = 0u;
+            if ((word >> sh) & 1u) { v0 = *reinterpret_cast<const uint16_t*>(smem_raw + r); r += 2u; }
+            if ((word >> (sh + 1)) & 1u) { v1 = *reinterpret_cast<const uint16_t*>(smem_raw + r); r += 2u; }
+            if ((word >> (sh + 2)) & 1u) { v2 = *reinterpret_cast<const uint16_t*>(smem_raw + r); r += 2u; }
+            if ((word >> (sh + 3)) & 1u) { v3 = *reinterpret_cast<const uint16_t*>(smem_raw + r); }
+            packed[2 * i] = __byte_perm(v0, v1, 0x5410);
+            packed[2 * i + 1] = __byte_perm(v2, v3, 0x5410);
           }
-          SALR_TMEM_ST_X8(taddr + 8u * c, packed);
+          SALR_TMEM_ST_X8(taddr + 8u * c4, packed);
         }
         tc_wait_st();
       }
@@ -1097,8 +1061,8 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     p.trace = g_trace;
   }
   {
-    p.rec_slot = (max_record_bytes > 0 && max_record_bytes <= kMaxRecordBytesBf16)
-                     ? (uint32_t)((max_record_bytes + 15) & ~15ll) : (uint32_t)kMaxRecordBytesBf16;
+    p.rec_slot = (max_record_bytes > 0 && max_record_bytes <= kMaxRecordBytesT2)
+                     ? (uint32_t)((max_record_bytes + 15) & ~15ll) : (uint32_t)kMaxRecordBytesT2;
     const int smax = max_stages(bm, ra, p.rec_slot);
     p.stages = stages <= 0 || stages > smax ? smax : stages;
   }

@@ -169,7 +169,7 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     _lib.require_cuda()
     if not isinstance(s, BitmapSparseMatrix):
         raise SalrError("s must be a BitmapSparseMatrix")
-    sb = s.to_bf16()
+    rec2, off2, max_rec2 = s.compute_format()
     xb = _prep_x(x, s.rows, check_finite)
     M = int(xb.shape[0])
     N = s.cols
@@ -192,8 +192,7 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     else:
         ws = workspace
     _lib.check(_lib.load().salr_linear_forward(
-        _lib.ptr(xb), M, s.rows, int(xb.shape[1]), _lib.ptr(sb.records), _lib.ptr(sb.tile_off),
-        sb.max_record_bytes, N,
+        _lib.ptr(xb), M, s.rows, int(xb.shape[1]), _lib.ptr(rec2), _lib.ptr(off2), max_rec2, N,
         _lib.ptr(acat), _lib.ptr(bct), r_pad, _lib.ptr(out), _lib.dtype_code(out.dtype), N,
         _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), 1 if pdl else 0, _lib.stream_ptr()))
     return out

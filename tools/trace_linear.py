@@ -29,6 +29,7 @@ g = torch.Generator(device="cuda").manual_seed(0)
 w = (torch.randn(K, N, generator=g, device="cuda") * 0.02).bfloat16()
 w = torch.where(w.float().abs() < 0.02 * 0.6744897501960817, torch.zeros_like(w), w)
 s = S.encode(w, value_dtype="bf16")
+s.compute_format()
 f = None if a.no_adapters else S.fuse([
     S.AdapterPair(torch.randn(K, 16, device="cuda") / 64, torch.randn(16, N, device="cuda") * 0.02, 16),
     S.AdapterPair(torch.randn(K, 16, device="cuda") / 64, torch.randn(16, N, device="cuda") * 0.02, 16, 2.0)])
