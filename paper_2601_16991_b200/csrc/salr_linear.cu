@@ -417,11 +417,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (int j = 0; j < 4; ++j) e[j] -= c[j];
         const uint32_t vbase = (uint32_t)(rec - smem_raw) + kT2Val + 2u * goff;
 #pragma unroll
+        for (int pp = 0; pp < WPG / 4; ++pp) {  // this warp's part, unrolled so bands are compile-time
+          if (pp != part) continue;
+#pragma unroll
         for (int c4 = 0; c4 < BPW / 4; ++c4) {  // 4 bands -> 8 TMEM columns
           uint32_t packed[8];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            const int b = BPW * part + 4 * c4 + i;  // compile-time when part == 0
+            const int b = BPW * pp + 4 * c4 + i;
             const uint32_t ev = e[(b >= 8 ? 2 : 0) + (b & 1)];
             const uint32_t ex = (ev >> (8 * ((b & 7) >> 1))) & 0xFFu;
             const uint32_t bov = (bo[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
@@ -437,6 +440,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             packed[2 * i + 1] = __byte_perm(v2, v3, 0x5410);
           }
           SALR_TMEM_ST_X8(taddr + 8u * c4, packed);
+        }
         }
         tc_wait_st();
       }
