@@ -70,6 +70,7 @@ struct LinearParams {
   uint32_t* ctrl;              // adapter control words (fixed workspace offset)
   int y_dtype;
   int stages;         // ring slots in use
+  int coop;           // 1: grid <= SM count, split tiles are reduced cooperatively
   uint32_t rec_slot;  // bytes per ring slot: the largest record of this matrix, 16-aligned
   int dbg;            // timing experiments only: 1 = skip decode, 2 = skip record loads
   unsigned long long* trace;  // optional per-CTA event timestamps (globaltimer ns), [G][32]
@@ -84,6 +85,7 @@ constexpr int kUFrac = 26;
 // ctrl words: [0] epoch (parity selects the U buffer), [1] done counter,
 // [2..3] u_ready[parity], [4..5] used elements of u_acc[parity]
 constexpr int kCtrlEpoch = 0, kCtrlDone = 1, kCtrlReady = 2, kCtrlUsed = 4;
+constexpr int kDoneTicketOff = 16 * 1024;  // second counter per split tile (workspace ticket area)
 constexpr int kUAccElems = 256 * 128;  // per parity buffer: M <= 256 rows x r_pad <= 128
 constexpr int kNumDecWarps = 16;
 constexpr int kNumThreads = 800;               // 25 warps
@@ -133,6 +135,11 @@ __device__ __forceinline__ int cta_of(int u, int units, int ctas) {
 
 // acq_rel ticket: orders this thread's prior (fenced-by-CTA-barrier) writes
 // before the increment and the reads after it behind it, at GPU scope.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* addr) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t v) {
   uint32_t old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
@@ -647,6 +654,47 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       prep_adapter(next_ad);
       next_ad = next_first_k(next_ad + 1);
     }
+    // Sum the partial tiles of a split output tile (the unit range starting
+    // at tile_base) over CTAs c_first..c_last in that fixed order
+    // (deterministic); this CTA takes share `share` of `nshare` row slices.
+    auto reduce_split = [&](int tile_base, int share, int nshare, bool reset) {
+      const int nt = (tile_base / p.n_kt) % p.n_nt;
+      const int mc = tile_base / (p.n_kt * p.n_nt);
+      const int rows = min(BM, p.M - mc * BM);
+      const int c_first = cta_of(tile_base, p.units, G), c_last = cta_of(tile_base + p.n_kt - 1, p.units, G);
+      const int n2 = nt * kTileN + etid;
+      // CTA c > c_first begins inside this tile (its slot 0); c_first
+      // holds it in slot 1 unless its range starts exactly at the tile.
+      const int cb_first = (int)((int64_t)c_first * p.units / G);
+      const size_t tile_elems = (size_t)BM * kTileN;
+      const float* p_first =
+          p.partials + ((size_t)c_first * 2 + (cb_first >= tile_base ? 0 : 1)) * tile_elems + etid;
+      const float* p_rest = p.partials + etid;  // + (2 c) * tile_elems
+      const int r0 = share * rows / nshare, r1 = (share + 1) * rows / nshare;
+      for (int m0 = r0; m0 < r1; m0 += 8) {
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          acc[i] = (m0 + i < r1) ? __ldcg(p_first + (size_t)(m0 + i) * kTileN) : 0.0f;
+#pragma unroll 4
+        for (int c = c_first + 1; c <= c_last; ++c) {
+          const float* pt = p_rest + (size_t)c * 2 * tile_elems + (size_t)m0 * kTileN;
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (m0 + i < r1) acc[i] += __ldcg(pt + (size_t)i * kTileN);
+        }
+        if (n2 < p.N) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (m0 + i >= r1) break;
+            const size_t o = (size_t)(mc * BM + m0 + i) * p.ldy + n2;
+            if (p.y_dtype == kF32) static_cast<float*>(p.y)[o] = acc[i];
+            else static_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(acc[i]);
+          }
+        }
+      }
+      if (reset && etid == 0) p.tickets[mc * p.n_nt + nt] = 0u;
+    };
     int seg = 0;
     int u = u_begin;
     while (u < u_end) {
@@ -697,57 +745,51 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
 
       if (!full_cover) {
-        // stream-K fixup: the last CTA to finish this (m-chunk, n-tile) sums
-        // the partial tiles of CTAs c_first..c_last in that fixed order.
+        // publish this CTA's partial of a split output tile (no waiting here:
+        // the reduction runs after the CTA's last segment, see below)
         named_bar_sync(1, 128);  // all 128 partial columns stored (CTA scope)
-        const int a = tile_base;
-        const int c_first = cta_of(a, p.units, G), c_last = cta_of(a + p.n_kt - 1, p.units, G);
         if (etid == 0) {
+          const int c_first = cta_of(tile_base, p.units, G), c_last = cta_of(tile_base + p.n_kt - 1, p.units, G);
           // acq_rel at GPU scope publishes this CTA's partial (ordered before
           // by the CTA barrier + cumulativity) and acquires the others'.
           const uint32_t old = ticket_add_acq_rel(&p.tickets[mc * p.n_nt + nt], 1u);
-          *last_flag = (old + 1 == (uint32_t)(c_last - c_first + 1)) ? 1u : 0u;
+          if (!p.coop) *last_flag = (old + 1 == (uint32_t)(c_last - c_first + 1)) ? 1u : 0u;
         }
         named_bar_sync(1, 128);
-        if (*last_flag) {
-          // thread etid owns column n2; rows in register chunks of 16 so all
-          // loads of one partial tile are in flight together.  Summation order
-          // per element is c_first..c_last (deterministic).
-          const int n2 = nt * kTileN + etid;
-          // CTA c > c_first begins inside this tile (its slot 0); c_first
-          // holds it in slot 1 unless its range starts exactly at the tile.
-          const int cb_first = (int)((int64_t)c_first * p.units / G);
-          const size_t tile_elems = (size_t)BM * kTileN;
-          const float* p_first = p.partials + ((size_t)c_first * 2 + (cb_first >= a ? 0 : 1)) * tile_elems + etid;
-          const float* p_rest = p.partials + etid;  // + (2 c) * tile_elems
-          for (int m0 = 0; m0 < rows; m0 += 8) {
-            float acc[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              acc[i] = (m0 + i < rows) ? __ldcg(p_first + (size_t)(m0 + i) * kTileN) : 0.0f;
-#pragma unroll 4
-            for (int c = c_first + 1; c <= c_last; ++c) {
-              const float* pt = p_rest + (size_t)c * 2 * tile_elems + (size_t)m0 * kTileN;
-#pragma unroll
-              for (int i = 0; i < 8; ++i)
-                if (m0 + i < rows) acc[i] += __ldcg(pt + (size_t)i * kTileN);
-            }
-            if (n2 < p.N) {
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                if (m0 + i >= rows) break;
-                const size_t o = (size_t)(mc * BM + m0 + i) * p.ldy + n2;
-                if (p.y_dtype == kF32) static_cast<float*>(p.y)[o] = acc[i];
-                else static_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(acc[i]);
-              }
-            }
-          }
-          if (etid == 0) p.tickets[mc * p.n_nt + nt] = 0u;
-        }
+        if (!p.coop && *last_flag) reduce_split(tile_base, 0, 1, true);
         named_bar_sync(1, 128);
       }
       ++seg;
       u = seg_end;
+    }
+    if (p.coop && u_begin < u_end) {
+      // Cooperative reduction of this CTA's split tiles (at most its first
+      // and its last segment), after all of its own partials are out: wait
+      // until every participant has published, then reduce our row share.
+      const int tiles[2] = {u_begin - u_begin % p.n_kt, (u_end - 1) - (u_end - 1) % p.n_kt};
+      for (int j = 0; j < 2; ++j) {
+        const int tb = tiles[j];
+        if (j == 1 && tb == tiles[0]) break;
+        const bool split = !(u_begin <= tb && tb + p.n_kt <= u_end);
+        if (!split) continue;
+        const int c_first = cta_of(tb, p.units, G), c_last = cta_of(tb + p.n_kt - 1, p.units, G);
+        const int np = c_last - c_first + 1;
+        const int nt = (tb / p.n_kt) % p.n_nt, mc = tb / (p.n_kt * p.n_nt);
+        uint32_t* tk = &p.tickets[mc * p.n_nt + nt];
+        if (etid == 0)
+          while (ld_acquire_u32(tk) < (uint32_t)np) __nanosleep(64);
+        named_bar_sync(1, 128);
+        reduce_split(tb, (int)blockIdx.x - c_first, np, false);
+        named_bar_sync(1, 128);
+        if (etid == 0) {
+          // the last participant out resets both counters for the next launch
+          uint32_t* dn = tk + kDoneTicketOff;
+          if (atomicAdd(dn, 1u) + 1 == (uint32_t)np) {
+            *tk = 0u;
+            *dn = 0u;
+          }
+        }
+      }
     }
     if (etid == 0) SALR_TRACE(8);
   }
@@ -964,7 +1006,7 @@ static inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 // the scratch regions (U hi/lo, U k-split partials, split-K partial tiles)
 // follow.
 constexpr size_t kTicketBytes = 256 * 1024;
-constexpr int64_t kMaxTileTickets = 32 * 1024, kMaxUTickets = 16 * 1024;
+constexpr int64_t kMaxTileTickets = 16 * 1024, kMaxUTickets = 16 * 1024;
 constexpr size_t kCtrlOff = kTicketBytes - 64;                 // adapter control words
 constexpr size_t kUAccOff = kTicketBytes;                      // 2 parity buffers, fixed place
 constexpr size_t kUAccBytes = 2 * (size_t)kUAccElems * 8;
@@ -1098,6 +1140,9 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   // in-kernel U needs every CTA resident at once (they wait on each other's
   // partials): one CTA per SM, grid <= SM count
   p.u_mode = ra ? ((M <= 256 && ctas <= sm_count()) ? 1 : 2) : 0;
+  // cooperative split-tile reduction pays off once a partial tile has rows
+  // to share (M >= 16); tiny ones stay with the last CTA (one round trip)
+  p.coop = (ctas <= sm_count() && M >= 16) ? 1 : 0;
   p.K = (int)K;
   p.x = static_cast<const __nv_bfloat16*>(x);
   p.acat = static_cast<const __nv_bfloat16*>(acat);
