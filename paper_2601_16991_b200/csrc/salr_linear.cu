@@ -304,6 +304,124 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (threadIdx.x == 0) SALR_TRACE(0);
   const uint32_t a_col0 = (uint32_t)((NACC * ACOLS + 31) & ~31);  // first A-stage column
 
+  // ---- in-kernel U = X @ A_cat (u_mode 1): this CTA's K-slice partial, added
+  // to the int64 fixed-point accumulator.  Run by the decoder and epilogue
+  // warps together (640 threads) while the first records are still in
+  // flight, so it costs (almost) nothing on the critical path.
+  // Long (decode-bound) launches leave it to the epilogue warps alone.
+  const bool u_wide = (u_end - u_begin) < 24;
+  const int kUThreads = u_wide ? 640 : 128;
+  const int kURowGroups = kUThreads / 64;
+  if (p.u_mode == 1 && warp >= (u_wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4) {
+    const int ut = (warp - (u_wide ? kFirstDecWarp : kFirstEpiWarp)) * 32 + (int)lane;
+    const int rp = 64 * p.ra;
+      pdl_wait();  // X may be the preceding kernel's output
+      const uint32_t par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
+      unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
+      // K slices on 8-element boundaries (16-byte rows for the staged loads)
+      const int k8 = (p.K % 8 == 0) ? 8 : 1, kq = p.K / k8;
+      const int k0 = k8 * (int)((int64_t)blockIdx.x * kq / G), k1 = k8 * (int)((int64_t)(blockIdx.x + 1) * kq / G);
+      // Stage the K slice of A_cat (ks x rp bf16) and row chunks of X
+      // (MCH x ks bf16) in the (still unused) adapter slot with coalesced
+      // 16-byte loads, so the FMA loop runs from shared memory instead of
+      // paying a global-load latency per k.
+      const int ks = k1 - k0;
+      const uint32_t slot_bytes = (uint32_t)p.ra * (kAdTileBytes + 2u * BM * 128u);
+      const uint32_t a_bytes = ((uint32_t)ks * rp * 2u + 15u) & ~15u;
+      const int mch = BM;  // rows per X chunk
+      const bool staged = ks > 0 && (p.K % 8 == 0) && (k0 % 8 == 0) && (ks % 8 == 0) &&
+                          a_bytes + (uint32_t)mch * ks * 2u <= slot_bytes;
+      const int rg = ut >> 6;  // row group 0..kURowGroups-1
+      if (staged) {
+        __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(adbuf);
+        __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(adbuf + a_bytes);
+        {  // A slice rows k0..k1 are contiguous in A_cat
+          const uint4* src = reinterpret_cast<const uint4*>(p.acat + (size_t)k0 * rp);
+          uint4* dst = reinterpret_cast<uint4*>(sa);
+          for (int i = ut; i < ks * rp / 8; i += kUThreads) dst[i] = __ldg(src + i);
+        }
+        for (int m0 = 0; m0 < p.M; m0 += mch) {
+          const int rows = min(mch, p.M - m0);
+          named_bar_sync(3, kUThreads);  // previous chunk consumed
+          for (int i = ut; i < rows * (ks / 8); i += kUThreads) {
+            const int m = i / (ks / 8), c = i % (ks / 8);
+            reinterpret_cast<uint4*>(sx + (size_t)m * ks)[c] =
+                __ldg(reinterpret_cast<const uint4*>(p.x + (size_t)(m0 + m) * p.ldx + k0) + c);
+          }
+          named_bar_sync(3, kUThreads);
+          for (int a = 0; a < p.ra; ++a) {
+            const int r = 64 * a + (ut & 63);
+            for (int mb = rg; mb < rows; mb += 8 * kURowGroups) {
+              float acc[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll 4
+              for (int k = 0; k < ks; ++k) {
+                const float av = __bfloat162float(sa[k * rp + r]);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const int m = mb + kURowGroups * i;
+                  if (m < rows) acc[i] = fmaf(__bfloat162float(sx[m * ks + k]), av, acc[i]);
+                }
+              }
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int m = mb + kURowGroups * i;
+                if (m < rows)
+                  atomicAdd(uacc + (size_t)(m0 + m) * rp + r,
+                            (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
+              }
+            }
+          }
+        }
+        named_bar_sync(3, kUThreads);  // slot free again for the adapter operands
+      } else {
+        for (int a = 0; a < p.ra; ++a) {
+          const int r = 64 * a + (ut & 63);
+          for (int mb = rg; mb < p.M; mb += 8 * kURowGroups) {
+            float acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+#pragma unroll 4
+            for (int k = k0; k < k1; ++k) {
+              const float av = __bfloat162float(p.acat[(size_t)k * rp + r]);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int m = mb + kURowGroups * i;
+                if (m < p.M) acc[i] = fmaf(__bfloat162float(p.x[(size_t)m * p.ldx + k]), av, acc[i]);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int m = mb + kURowGroups * i;
+              if (m < p.M && k1 > k0)
+                atomicAdd(uacc + (size_t)m * rp + r,
+                          (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
+            }
+          }
+        }
+      }
+      // the previous adapter launch's buffer (other parity) is idle in this
+      // launch: CTA 0 clears it for the next one
+      if (blockIdx.x == 0) {
+        // the previous user of that buffer may have had another shape: clear
+        // exactly the prefix it recorded as used
+        unsigned long long* other = p.u_acc + (size_t)(par ^ 1u) * kUAccElems;
+        const uint32_t used = p.ctrl[kCtrlUsed + (par ^ 1u)];
+        for (uint32_t i = (uint32_t)ut; i < used; i += kUThreads) other[i] = 0ull;
+        if (ut == 0) {
+          p.ctrl[kCtrlReady + (par ^ 1u)] = 0u;
+          p.ctrl[kCtrlUsed + (par ^ 1u)] = 0u;
+          p.ctrl[kCtrlUsed + par] = (uint32_t)(p.M * rp);
+        }
+      }
+      named_bar_sync(3, kUThreads);
+      if (ut == 0) {
+        __threadfence();
+        atomicAdd(p.ctrl + kCtrlReady + par, 1u);
+      }
+  }
+
   if (warp == kWarpProd0 || warp == kWarpProd1) {
     // ================= TMA producers
     if (lane == 0 && pk == 0) SALR_TRACE(1);
@@ -469,114 +587,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int etid = (warp - kFirstEpiWarp) * 32 + (int)lane;  // 0..127
     const int rp = 64 * p.ra;
     uint32_t par = 0;
-    if (p.u_mode == 1) {
-      // ---- this CTA's K-slice partial of U = X @ A_cat -> int64 atomics
-      pdl_wait();  // X may be the preceding kernel's output
-      par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
-      unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
-      // K slices on 8-element boundaries (16-byte rows for the staged loads)
-      const int k8 = (p.K % 8 == 0) ? 8 : 1, kq = p.K / k8;
-      const int k0 = k8 * (int)((int64_t)blockIdx.x * kq / G), k1 = k8 * (int)((int64_t)(blockIdx.x + 1) * kq / G);
-      // Stage the K slice of A_cat (ks x rp bf16) and row chunks of X
-      // (MCH x ks bf16) in the (still unused) adapter slot with coalesced
-      // 16-byte loads, so the FMA loop runs from shared memory instead of
-      // paying a global-load latency per k.
-      const int ks = k1 - k0;
-      const uint32_t slot_bytes = (uint32_t)p.ra * (kAdTileBytes + 2u * BM * 128u);
-      const uint32_t a_bytes = ((uint32_t)ks * rp * 2u + 15u) & ~15u;
-      const int mch = BM;  // rows per X chunk
-      const bool staged = ks > 0 && (p.K % 8 == 0) && (k0 % 8 == 0) && (ks % 8 == 0) &&
-                          a_bytes + (uint32_t)mch * ks * 2u <= slot_bytes;
-      const int mh = etid >> 6;
-      if (staged) {
-        __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(adbuf);
-        __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(adbuf + a_bytes);
-        {  // A slice rows k0..k1 are contiguous in A_cat
-          const uint4* src = reinterpret_cast<const uint4*>(p.acat + (size_t)k0 * rp);
-          uint4* dst = reinterpret_cast<uint4*>(sa);
-          for (int i = etid; i < ks * rp / 8; i += 128) dst[i] = __ldg(src + i);
-        }
-        for (int m0 = 0; m0 < p.M; m0 += mch) {
-          const int rows = min(mch, p.M - m0);
-          named_bar_sync(1, 128);  // previous chunk consumed
-          for (int i = etid; i < rows * (ks / 8); i += 128) {
-            const int m = i / (ks / 8), c = i % (ks / 8);
-            reinterpret_cast<uint4*>(sx + (size_t)m * ks)[c] =
-                __ldg(reinterpret_cast<const uint4*>(p.x + (size_t)(m0 + m) * p.ldx + k0) + c);
-          }
-          named_bar_sync(1, 128);
-          for (int a = 0; a < p.ra; ++a) {
-            const int r = 64 * a + (etid & 63);
-            for (int mb = mh; mb < rows; mb += 16) {
-              float acc[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-#pragma unroll 4
-              for (int k = 0; k < ks; ++k) {
-                const float av = __bfloat162float(sa[k * rp + r]);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const int m = mb + 2 * i;
-                  if (m < rows) acc[i] = fmaf(__bfloat162float(sx[m * ks + k]), av, acc[i]);
-                }
-              }
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int m = mb + 2 * i;
-                if (m < rows)
-                  atomicAdd(uacc + (size_t)(m0 + m) * rp + r,
-                            (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
-              }
-            }
-          }
-        }
-        named_bar_sync(1, 128);  // slot free again for the adapter operands
-      } else {
-        for (int a = 0; a < p.ra; ++a) {
-          const int r = 64 * a + (etid & 63);
-          for (int mb = mh; mb < p.M; mb += 16) {
-            float acc[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-#pragma unroll 4
-            for (int k = k0; k < k1; ++k) {
-              const float av = __bfloat162float(p.acat[(size_t)k * rp + r]);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int m = mb + 2 * i;
-                if (m < p.M) acc[i] = fmaf(__bfloat162float(p.x[(size_t)m * p.ldx + k]), av, acc[i]);
-              }
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int m = mb + 2 * i;
-              if (m < p.M && k1 > k0)
-                atomicAdd(uacc + (size_t)m * rp + r,
-                          (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
-            }
-          }
-        }
-      }
-      // the previous adapter launch's buffer (other parity) is idle in this
-      // launch: CTA 0 clears it for the next one
-      if (blockIdx.x == 0) {
-        // the previous user of that buffer may have had another shape: clear
-        // exactly the prefix it recorded as used
-        unsigned long long* other = p.u_acc + (size_t)(par ^ 1u) * kUAccElems;
-        const uint32_t used = p.ctrl[kCtrlUsed + (par ^ 1u)];
-        for (uint32_t i = (uint32_t)etid; i < used; i += 128) other[i] = 0ull;
-        if (etid == 0) {
-          p.ctrl[kCtrlReady + (par ^ 1u)] = 0u;
-          p.ctrl[kCtrlUsed + (par ^ 1u)] = 0u;
-          p.ctrl[kCtrlUsed + par] = (uint32_t)(p.M * rp);
-        }
-      }
-      named_bar_sync(1, 128);
-      if (etid == 0) {
-        __threadfence();
-        atomicAdd(p.ctrl + kCtrlReady + par, 1u);
-      }
-    }
+    if (p.u_mode == 1) par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
     bool u_ok = false;
     uint32_t ad_ph = 0;
     // adapter operands of the output tile whose first k-unit is useg (a
