@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* ad_empty = ad_full + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ad_empty + 1);
   volatile uint32_t* last_flag = tmem_slot + 1;
+  uint32_t* zero_word = tmem_slot + 2;  // a shared zero the decoders load for absent elements
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
       mbar_init(ad_full, 1);
       mbar_init(ad_empty, 1);
+      *zero_word = 0u;
       fence_barrier_init();
     }
     named_bar_sync(2, 64);  // barriers initialised before either producer uses them
@@ -540,7 +542,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) e[j] -= c[j];
-        const uint32_t vbase = (uint32_t)(rec - smem_raw) + kT2Val + 2u * goff;
+        const uint32_t vbase = smem_u32(rec) + kT2Val + 2u * goff;
 #pragma unroll
         for (int pp = 0; pp < WPG / 4; ++pp) {  // this warp's part, unrolled so bands are compile-time
           if (pp != part) continue;
@@ -556,11 +558,23 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             uint32_t r = vbase + 2u * (bov + ex);
             const uint32_t word = b < 8 ? mw.x : mw.y;
             const int sh = 4 * (b & 7);
+            // predicated pointer chain: @p ld.shared + @p add, per element
             uint32_t v0 = 0u, v1 = 0u, v2 = 0u, v3 = 0u;
-            if ((word >> sh) & 1u) { v0 = *reinterpret_cast<const uint16_t*>(smem_raw + r); r += 2u; }
-            if ((word >> (sh + 1)) & 1u) { v1 = *reinterpret_cast<const uint16_t*>(smem_raw + r); r += 2u; }
-            if ((word >> (sh + 2)) & 1u) { v2 = *reinterpret_cast<const uint16_t*>(smem_raw + r); r += 2u; }
-            if ((word >> (sh + 3)) & 1u) { v3 = *reinterpret_cast<const uint16_t*>(smem_raw + r); }
+            asm volatile(
+                "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
+                "setp.ne.b32 q0, %5, 0;\n\t"
+                "setp.ne.b32 q1, %6, 0;\n\t"
+                "setp.ne.b32 q2, %7, 0;\n\t"
+                "setp.ne.b32 q3, %8, 0;\n\t"
+                "@q0 ld.shared.u16 %0, [%4];\n\t"
+                "@q0 add.u32 %4, %4, 2;\n\t"
+                "@q1 ld.shared.u16 %1, [%4];\n\t"
+                "@q1 add.u32 %4, %4, 2;\n\t"
+                "@q2 ld.shared.u16 %2, [%4];\n\t"
+                "@q2 add.u32 %4, %4, 2;\n\t"
+                "@q3 ld.shared.u16 %3, [%4];\n\t}"
+                : "+r"(v0), "+r"(v1), "+r"(v2), "+r"(v3), "+r"(r)
+                : "r"(word & (1u << sh)), "r"(word & (2u << sh)), "r"(word & (4u << sh)), "r"(word & (8u << sh)));
             packed[2 * i] = __byte_perm(v0, v1, 0x5410);
             packed[2 * i + 1] = __byte_perm(v2, v3, 0x5410);
           }

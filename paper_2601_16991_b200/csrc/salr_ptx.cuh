@@ -106,6 +106,15 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// 16-bit shared-memory load by 32-bit shared address, zero-extended.
+// volatile: stays ordered after the (volatile) mbarrier waits that publish
+// the TMA-written data.
+__device__ __forceinline__ uint32_t lds_u16(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
+}
+
 // ---------------------------------------------------------------- TMA
 // 1-D bulk copy global -> shared, completion on an mbarrier (complete_tx).
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,
