@@ -311,7 +311,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // warps together (640 threads) while the first records are still in
   // flight, so it costs (almost) nothing on the critical path.
   // Long (decode-bound) launches leave it to the epilogue warps alone.
-  const bool u_wide = (u_end - u_begin) < 24;
+  // (With few tokens the partial is latency-, not work-bound: keep the
+  // decoders out of it.)
+  const bool u_wide = (u_end - u_begin) < 24 && p.M >= 16;
   const int kUThreads = u_wide ? 640 : 128;
   const int kURowGroups = kUThreads / 64;
   if (p.u_mode == 1 && warp >= (u_wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4) {
