@@ -232,7 +232,8 @@ def cpu_sample(tokens: int, sparsity: float, budget_s: float = 20.0, prefer_refe
 
 def stack_config(args, world, how):
     return {"workload": "llama3-8b 32-layer SALR linear stack (q,k,v,o,gate,up,down; configs[1] shapes x32 "
-                        "layers = configs[3] at this N), one decode token-batch per step",
+                        "layers = configs[3] at this N), one decode token-batch per step; q|k|v and gate|up "
+                        "weights column-concatenated (4 SALR linears per layer, adapters per original linear)",
             "tokens": args.tokens, "layers": 32, "sparsity": args.sparsity, "adapters": "r16+r16 fused (R=32)",
             "parallelism": f"col-shard{world}" if world > 1 else "single",
             "l2": "working set 7.85 GB >> 126 MB L2 (inputs larger than L2)", "execution": how}
@@ -263,22 +264,34 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # the B200 arm
 
+# The stack runs the per-layer linears as four SALR linears: q|k|v and
+# gate|up share their input, so their weights are concatenated along the
+# output columns (one encode each; adapters keep their per-linear blocks,
+# B_cat is block-structured) -- mathematically the same seven linears with
+# one weight stream and one launch per shared input.
+FUSED = {"qkv": (4096, [("q", 4096), ("k", 1024), ("v", 1024)]),
+         "o": (4096, [("o", 4096)]),
+         "gateup": (4096, [("gate", 14336), ("up", 14336)]),
+         "down": (14336, [("down", 4096)])}
+STACK_ORDER = ("qkv", "o", "gateup", "down")
+
+
 def build_stack(layers, world, rank, sparsity, device):
-    """Per layer: {name: (BitmapSparseMatrix shard, FusedAdapters shard, (k, n_local), col range)}."""
+    """Per layer: {fused name: (BitmapSparseMatrix shard, FusedAdapters shard, (k, n_local), col range)}."""
     import torch
     import paper_2601_16991_b200 as S
 
     g = torch.Generator(device=device).manual_seed(1234 + 17 * rank)
-    thr = 0.02 * 0.6744897501960817  # N(0, 0.02^2) |w| median: prunes 50% by magnitude
     q = {0.3: 0.3853204664075676, 0.5: 0.6744897501960817, 0.7: 1.0364333894937898}.get(sparsity)
     if q is None:
         raise SystemExit(f"unsupported sparsity {sparsity}")
-    thr = 0.02 * q
+    thr = 0.02 * q  # |w| quantile of N(0, 0.02^2): magnitude pruning at `sparsity`
     stack = []
     for layer in range(layers):
         lin = {}
-        for name in LINEARS:
-            k, n = SHAPES[name]
+        for name in STACK_ORDER:
+            k, parts = FUSED[name]
+            n = sum(w for _, w in parts)
             c0, c1 = shard_cols(n, world, rank)
             nl = c1 - c0
             w = (torch.randn(k, nl, generator=g, device=device) * 0.02).to(torch.bfloat16)
@@ -286,10 +299,17 @@ def build_stack(layers, world, rank, sparsity, device):
             s = S.encode(w, value_dtype="bf16")
             s.compute_format()  # the linear kernel's operand format, built once at load
             del w
-            ads = [S.AdapterPair((torch.randn(k, 16, generator=g, device=device) / 64).bfloat16().float(),
-                                 (torch.randn(16, nl, generator=g, device=device) * 0.02).bfloat16().float(), 16),
-                   S.AdapterPair((torch.randn(k, 16, generator=g, device=device) / 64).bfloat16().float(),
-                                 (torch.randn(16, nl, generator=g, device=device) * 0.02).bfloat16().float(), 16, 2.0)]
+            ads = []
+            p0 = 0
+            for _, pw in parts:  # LoRA r16 + residual r16 per original linear, on its own columns
+                lo, hi = max(p0, c0) - c0, min(p0 + pw, c1) - c0
+                for scale in (1.0, 2.0):
+                    a = (torch.randn(k, 16, generator=g, device=device) / 64).bfloat16().float()
+                    bm = torch.zeros(16, nl, device=device)
+                    if hi > lo:
+                        bm[:, lo:hi] = (torch.randn(16, hi - lo, generator=g, device=device) * 0.02).bfloat16().float()
+                    ads.append(S.AdapterPair(a, bm, 16, scale))
+                p0 += pw
             fused = S.fuse(ads)
             fused.device_operands()
             lin[name] = (s, fused, (k, nl), (c0, c1))
@@ -306,48 +326,35 @@ class StackRunner:
         self.S, self.stack, self.M, self.world, self.group = S, stack, tokens, world, group
         dev = torch.device("cuda", torch.cuda.current_device())
         self.x_in = torch.zeros(tokens, 4096, dtype=torch.bfloat16, device=dev)
-        self.bufs = {}
-        for name in LINEARS:
-            k, n = SHAPES[name]
-            nl = stack[0][name][2][1]
-            self.bufs[name] = torch.empty(tokens, nl, dtype=torch.bfloat16, device=dev)
-        self.full = {w: torch.empty(tokens, w, dtype=torch.bfloat16, device=dev) for w in (4096, 14336, 6144, 28672)}
+        self.bufs = {name: torch.empty(tokens, stack[0][name][2][1], dtype=torch.bfloat16, device=dev)
+                     for name in STACK_ORDER}
         self.launches_per_step = 0
 
-    def _gather(self, locals_, widths):
-        """All-gather column shards of one or more linears into full rows."""
+    def _gather(self, local, width):
+        """All-gather the column shards of one linear into full rows."""
         if self.world == 1:
-            return locals_
+            return local
         from paper_2601_16991_b200.sharding import gather_columns
-        return [gather_columns(t, w, group=self.group) for t, w in zip(locals_, widths)]
+        return gather_columns(local, width, group=self.group)
+
+    def _linear(self, x, lin, name):
+        s, f, _, _ = lin[name]
+        y = self.S.salr_linear(x, s, f, out=self.bufs[name], check_finite=False, pdl=True)
+        # one fused kernel per linear (M <= 256: U = X @ A_cat is computed in-kernel)
+        self._launches += 1 if self.M <= 256 else 2
+        return self._gather(y, sum(w for _, w in FUSED[name][1]))
 
     def step(self, x):
-        S = self.S
+        self._launches = 0
         h = x
-        launches = 0
         for lin in self.stack:
-            outs = {}
-            for name in ("q", "k", "v"):
-                s, f, _, _ = lin[name]
-                outs[name] = S.salr_linear(h, s, f, out=self.bufs[name], check_finite=False, pdl=True)
-                launches += 2
-            q, _, _ = self._gather([outs["q"], outs["k"], outs["v"]], [4096, 1024, 1024])
-            s, f, _, _ = lin["o"]
-            o = S.salr_linear(q, s, f, out=self.bufs["o"], check_finite=False, pdl=True)
-            launches += 2
-            (o,) = self._gather([o], [4096])
-            for name in ("gate", "up"):
-                s, f, _, _ = lin[name]
-                outs[name] = S.salr_linear(o, s, f, out=self.bufs[name], check_finite=False, pdl=True)
-                launches += 2
-            # the stack is linears only (the MLP nonlinearity is outside the hot
-            # path): down consumes the gathered gate projection
-            gate, _ = self._gather([outs["gate"], outs["up"]], [14336, 14336])
-            s, f, _, _ = lin["down"]
-            d = S.salr_linear(gate, s, f, out=self.bufs["down"], check_finite=False, pdl=True)
-            launches += 2
-            (h,) = self._gather([d], [4096])
-        self.launches_per_step = launches
+            qkv = self._linear(h, lin, "qkv")
+            # the stack is linears only (attention is outside the hot path):
+            # o consumes the q columns, down the gate columns
+            o = self._linear(qkv[:, :4096], lin, "o")
+            gu = self._linear(o, lin, "gateup")
+            h = self._linear(gu[:, :14336], lin, "down")
+        self.launches_per_step = self._launches
         return h
 
 
@@ -411,7 +418,7 @@ def per_linear_kernel_times(stack, tokens, reps=32):
     x = {4096: torch.randn(tokens, 4096, device="cuda").bfloat16(),
          14336: torch.randn(tokens, 14336, device="cuda").bfloat16()}
     L = len(stack)
-    for name in LINEARS:
+    for name in STACK_ORDER:
         k, nl = stack[0][name][2]
         outs = [torch.empty(tokens, nl, dtype=torch.bfloat16, device="cuda") for _ in range(2)]
 
@@ -431,7 +438,7 @@ def cublas_times(stack, tokens, reps=20):
     import paper_2601_16991_b200 as S
     res = {}
     L = min(len(stack), 8)
-    for name in LINEARS:
+    for name in STACK_ORDER:
         k, nl = stack[0][name][2]
         ws = []
         for i in range(L):
@@ -478,7 +485,7 @@ def run_salr(args):
     ms_per_step = ms / args.steps
     tokens_per_s = M / (ms_per_step / 1e3)  # every rank processes the same M tokens (sharded columns)
 
-    comp_bytes_local = sum(lin[n][0].compressed_bytes for lin in stack for n in LINEARS)
+    comp_bytes_local = sum(lin[n][0].compressed_bytes for lin in stack for n in STACK_ORDER)
     comp_bytes = comp_bytes_local
     if world > 1:
         t = torch.tensor([float(comp_bytes_local)], device=dev)
