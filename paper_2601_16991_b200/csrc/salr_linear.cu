@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // Long (decode-bound) launches leave it to the epilogue warps alone.
   // (With few tokens the partial is latency-, not work-bound: keep the
   // decoders out of it.)
-  const bool u_wide = (u_end - u_begin) < 24 && p.M >= 16;
+  const bool u_wide = (p.dbg & 4) ? false : ((u_end - u_begin) < 24 && p.M >= 16);
   const int kUThreads = u_wide ? 640 : 128;
   const int kURowGroups = kUThreads / 64;
   if (p.u_mode == 1 && warp >= (u_wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4) {
@@ -1162,6 +1162,20 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   // fixup for a pipeline that never fills.
   constexpr int64_t kMinUnitsPerCta = 6;
   int64_t ctas = num_ctas > 0 ? num_ctas : std::min<int64_t>(sm_count(), (p.units + kMinUnitsPerCta - 1) / kMinUnitsPerCta);
+  if (num_ctas <= 0 && M >= 16 && !(getenv("SALR_NO_ALIGNED_GRID"))) {
+    // Prefer a grid (>= 6/7 of the SMs) whose per-CTA unit ranges tile the
+    // K dimension exactly: every split output tile is then shared by
+    // CTAs that finish together, so the split-K reduction does not wait on
+    // a straggler (q/o/k/v/down at M >= 16, where the reduction is heavy).
+    for (int64_t c = ctas; c >= (6 * ctas + 6) / 7; --c) {
+      if (p.units % c) continue;
+      const int64_t per = p.units / c;
+      if (p.n_kt % per == 0 || per % p.n_kt == 0) {
+        ctas = c;
+        break;
+      }
+    }
+  }
   if (ctas > p.units) ctas = p.units;
   SALR_CHECK_ARG(ctas <= 65535, SALR_ERR_CONFIG, "num_ctas too large");
   // in-kernel U needs every CTA resident at once (they wait on each other's

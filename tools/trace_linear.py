@@ -23,6 +23,7 @@ ap.add_argument("--shape", default="gate")
 ap.add_argument("--tokens", type=int, default=1)
 ap.add_argument("--no-adapters", action="store_true")
 ap.add_argument("--launches", type=int, default=4)
+ap.add_argument("--graph", action="store_true", help="capture the launches (PDL-chained) in one CUDA graph")
 a = ap.parse_args()
 K, N = synthetic.LLAMA3_8B_LINEARS[a.shape]
 g = torch.Generator(device="cuda").manual_seed(0)
@@ -41,17 +42,31 @@ torch.cuda.synchronize()
 bufs = [torch.zeros(148 * 32 + 16 * 64, dtype=torch.int64, device="cuda") for _ in range(a.launches)]
 gr = torch.cuda.CUDAGraph()
 lib = _lib.load()
-# launches are recorded eagerly back to back (trace pointer is baked per launch)
-for b in bufs:
-    lib.salr_debug_set_trace(_lib.ptr(b))
-    S.salr_linear(x, s, f, out=out, check_finite=False)
-lib.salr_debug_set_trace(None)
-torch.cuda.synchronize()
+outs = [out, torch.empty_like(out)]
+if a.graph:
+    # the trace pointer is a kernel argument: baked per captured launch
+    with torch.cuda.graph(gr):
+        for i, b in enumerate(bufs):
+            lib.salr_debug_set_trace(_lib.ptr(b))
+            S.salr_linear(x, s, f, out=outs[i & 1], check_finite=False, pdl=True)
+    lib.salr_debug_set_trace(None)
+    for _ in range(3):
+        gr.replay()
+    torch.cuda.synchronize()
+else:
+    # launches are recorded eagerly back to back (trace pointer is baked per launch)
+    for b in bufs:
+        lib.salr_debug_set_trace(_lib.ptr(b))
+        S.salr_linear(x, s, f, out=out, check_finite=False)
+    lib.salr_debug_set_trace(None)
+    torch.cuda.synchronize()
 prev_end = None
 for i, b in enumerate(bufs):
     t = b[:148 * 32].view(148, 32).cpu()
     dd = b[148 * 32:].view(16, 64).cpu()
     t0 = int(t[:, 10][t[:, 10] > 0].min())
+    if prev_end is None and i == 0 and a.graph:
+        pass
     print(f"launch {i}: " + (f"gap from previous last cta end {(t0 - prev_end) / 1e3:.2f} us" if prev_end else ""))
     for ev, name in EV.items():
         col = t[:, ev]
