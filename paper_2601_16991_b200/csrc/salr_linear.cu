@@ -78,13 +78,15 @@ struct LinearParams {
   uint32_t x_off, rec_off, base_off, ad_off, bar_off;
 };
 
-// In-kernel U = X @ A_cat: every CTA adds the partial of its K slice into an
+// In-kernel U = X @ A_cat: CTAs claim K slices and add their partials into an
 // int64 fixed-point accumulator (2^-kUFrac resolution).  Integer addition is
 // associative, so U is bit-reproducible whatever the CTA order.
 constexpr int kUFrac = 26;
 // ctrl words: [0] epoch (parity selects the U buffer), [1] done counter,
-// [2..3] u_ready[parity], [4..5] used elements of u_acc[parity]
-constexpr int kCtrlEpoch = 0, kCtrlDone = 1, kCtrlReady = 2, kCtrlUsed = 4;
+// [2..3] slices done[parity], [4..5] used elements of u_acc[parity],
+// [6..7] slice claim counter[parity]
+constexpr int kCtrlEpoch = 0, kCtrlDone = 1, kCtrlReady = 2, kCtrlUsed = 4, kCtrlSlice = 6;
+constexpr int kUSlice = 64;  // K rows per dynamically claimed U slice
 constexpr int kDoneTicketOff = 16 * 1024;  // second counter per split tile (workspace ticket area)
 constexpr int kUAccElems = 256 * 128;  // per parity buffer: M <= 256 rows x r_pad <= 128
 constexpr int kNumDecWarps = 16;
@@ -306,79 +308,111 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (threadIdx.x == 0) SALR_TRACE(0);
   const uint32_t a_col0 = (uint32_t)((NACC * ACOLS + 31) & ~31);  // first A-stage column
 
-  // ---- in-kernel U = X @ A_cat (u_mode 1): this CTA's K-slice partial, added
-  // to the int64 fixed-point accumulator.  Run by the decoder and epilogue
-  // warps together (640 threads) while the first records are still in
-  // flight, so it costs (almost) nothing on the critical path.
-  // Long (decode-bound) launches leave it to the epilogue warps alone.
-  // (With few tokens the partial is latency-, not work-bound: keep the
-  // decoders out of it.)
+  // ---- in-kernel U = X @ A_cat (u_mode 1).  K is cut into slices of
+  // kUSlice rows that CTAs claim dynamically (atomic counter): CTAs that
+  // start early (programmatic launches start staggered) do the work, late
+  // ones find none left, so U is ready soon after the first CTAs start.
+  // Each slice partial goes into the int64 fixed-point accumulator (integer
+  // atomics: order-independent, bit-reproducible).  Participants: the
+  // epilogue warps, plus the decoder warps for short launches with M >= 16
+  // (work-bound partials); with few tokens it is latency-bound.
   const bool u_wide = (p.dbg & 4) ? false : ((u_end - u_begin) < 24 && p.M >= 16);
   const int kUThreads = u_wide ? 640 : 128;
   const int kURowGroups = kUThreads / 64;
   if (p.u_mode == 1 && warp >= (u_wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4) {
     const int ut = (warp - (u_wide ? kFirstDecWarp : kFirstEpiWarp)) * 32 + (int)lane;
     const int rp = 64 * p.ra;
-      pdl_wait();  // X may be the preceding kernel's output
-      const uint32_t par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
-      unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
-      // K slices on 8-element boundaries (16-byte rows for the staged loads)
-      const int k8 = (p.K % 8 == 0) ? 8 : 1, kq = p.K / k8;
-      const int k0 = k8 * (int)((int64_t)blockIdx.x * kq / G), k1 = k8 * (int)((int64_t)(blockIdx.x + 1) * kq / G);
-      // Stage the K slice of A_cat (ks x rp bf16) and row chunks of X
-      // (MCH x ks bf16) in the (still unused) adapter slot with coalesced
-      // 16-byte loads, so the FMA loop runs from shared memory instead of
-      // paying a global-load latency per k.
-      const int ks = k1 - k0;
-      const uint32_t slot_bytes = (uint32_t)p.ra * (kAdTileBytes + 2u * BM * 128u);
-      const uint32_t a_bytes = ((uint32_t)ks * rp * 2u + 15u) & ~15u;
-      const int mch = BM;  // rows per X chunk
-      const bool staged = ks > 0 && (p.K % 8 == 0) && (k0 % 8 == 0) && (ks % 8 == 0) &&
-                          a_bytes + (uint32_t)mch * ks * 2u <= slot_bytes;
-      const int rg = ut >> 6;  // row group 0..kURowGroups-1
+    pdl_wait();  // X may be the preceding kernel's output
+    const uint32_t par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
+    unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
+    if (ut == 0) SALR_TRACE(19);
+    if (blockIdx.x == 0) {
+      // the previous adapter launch's buffer (other parity) is idle in this
+      // launch: clear exactly the prefix its user recorded, reset its counters
+      unsigned long long* other = p.u_acc + (size_t)(par ^ 1u) * kUAccElems;
+      const uint32_t used = p.ctrl[kCtrlUsed + (par ^ 1u)];
+      for (uint32_t i = (uint32_t)ut; i < used; i += kUThreads) other[i] = 0ull;
+      if (ut == 0) {
+        p.ctrl[kCtrlReady + (par ^ 1u)] = 0u;
+        p.ctrl[kCtrlSlice + (par ^ 1u)] = 0u;
+        p.ctrl[kCtrlUsed + (par ^ 1u)] = 0u;
+        p.ctrl[kCtrlUsed + par] = (uint32_t)(p.M * rp);
+      }
+    }
+    const int nsl = (p.K + kUSlice - 1) / kUSlice;
+    // staged slices: A slice (kUSlice x rp, row stride rp+8) and an X row
+    // chunk (BM x kUSlice, row stride kUSlice+8; the pads make the mma
+    // fragment loads bank-conflict free) in the still unused adapter slot.
+    constexpr int kSX = kUSlice + 8;
+    const int kSA = rp + 8;
+    const uint32_t slot_bytes = (uint32_t)p.ra * (kAdTileBytes + 2u * BM * 128u);
+    const bool staged = (p.K % 8 == 0) && (uint32_t)(kUSlice * kSA + BM * kSX) * 2u <= slot_bytes;
+    __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(adbuf);
+    __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(adbuf + (uint32_t)kUSlice * kSA * 2u);
+    const int rg = ut >> 6;  // row group 0..kURowGroups-1 (scalar path)
+    uint32_t done = 0;
+    for (;;) {
+      if (ut == 0) *last_flag = atomicAdd(p.ctrl + kCtrlSlice + par, 1u);
+      named_bar_sync(3, kUThreads);
+      const int sl = (int)*last_flag;
+      named_bar_sync(3, kUThreads);
+      if (ut == 0 && done == 0) SALR_TRACE(15);
+      if (sl >= nsl) break;
+      const int k0 = sl * kUSlice, ks = min(kUSlice, p.K - k0);
       if (staged) {
-        __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(adbuf);
-        __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(adbuf + a_bytes);
-        {  // A slice rows k0..k1 are contiguous in A_cat
+        const int ks16 = (ks + 15) & ~15;  // zero-padded to whole mma k-steps
+        {  // A slice rows k0..k0+ks are contiguous in A_cat
           const uint4* src = reinterpret_cast<const uint4*>(p.acat + (size_t)k0 * rp);
-          uint4* dst = reinterpret_cast<uint4*>(sa);
-          for (int i = ut; i < ks * rp / 8; i += kUThreads) dst[i] = __ldg(src + i);
+          const int cpr = rp / 8;  // 16-byte chunks per row
+          for (int i = ut; i < ks16 * cpr; i += kUThreads) {
+            const int kr = i / cpr, c = i % cpr;
+            reinterpret_cast<uint4*>(sa + kr * kSA)[c] = kr < ks ? __ldg(src + i) : make_uint4(0u, 0u, 0u, 0u);
+          }
         }
-        for (int m0 = 0; m0 < p.M; m0 += mch) {
-          const int rows = min(mch, p.M - m0);
-          named_bar_sync(3, kUThreads);  // previous chunk consumed
-          for (int i = ut; i < rows * (ks / 8); i += kUThreads) {
-            const int m = i / (ks / 8), c = i % (ks / 8);
-            reinterpret_cast<uint4*>(sx + (size_t)m * ks)[c] =
-                __ldg(reinterpret_cast<const uint4*>(p.x + (size_t)(m0 + m) * p.ldx + k0) + c);
+        const int wid = ut >> 5, nw = kUThreads / 32;
+        const int g = (int)lane >> 2, t = (int)lane & 3;
+        const uint32_t sa_u = smem_u32(sa), sx_u = smem_u32(sx);
+        for (int m0 = 0; m0 < p.M; m0 += BM) {
+          const int rows = min(BM, p.M - m0);
+          if (m0) named_bar_sync(3, kUThreads);  // previous chunk consumed
+          for (int i = ut; i < rows * (ks16 / 8); i += kUThreads) {
+            const int m = i / (ks16 / 8), c = i % (ks16 / 8);
+            reinterpret_cast<uint4*>(sx + m * kSX)[c] =
+                c < ks / 8 ? __ldg(reinterpret_cast<const uint4*>(p.x + (size_t)(m0 + m) * p.ldx + k0) + c)
+                           : make_uint4(0u, 0u, 0u, 0u);
           }
           named_bar_sync(3, kUThreads);
-          for (int a = 0; a < p.ra; ++a) {
-            const int r = 64 * a + (ut & 63);
-            for (int mb = rg; mb < rows; mb += 8 * kURowGroups) {
-              float acc[8];
+          if (ut == 0 && done == 0 && m0 == 0) SALR_TRACE(16);
+          // (16-row block, 8-column block) items over the warps; rows past
+          // `rows` read stale shared memory and are never stored.
+          const int nnb = rp / 8, items = nnb * ((rows + 15) / 16);
+          for (int it = wid; it < items; it += nw) {
+            const int nb = it % nnb, mb = it / nnb;
+            float c[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int kk = 0; kk < ks16; kk += 16) {
+              uint32_t af[4], bf[2];
+              const uint32_t xa = sx_u + (uint32_t)(((mb * 16 + g) * kSX + kk + 2 * t) * 2);
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(af[0]) : "r"(xa));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(af[1]) : "r"(xa + 8 * kSX * 2));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(af[2]) : "r"(xa + 16));
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(af[3]) : "r"(xa + 8 * kSX * 2 + 16));
+              const uint32_t aa = sa_u + (uint32_t)(((kk + 2 * t) * kSA + nb * 8 + g) * 2);
+              bf[0] = lds_u16(aa) | (lds_u16(aa + kSA * 2) << 16);
+              bf[1] = lds_u16(aa + 8 * kSA * 2) | (lds_u16(aa + 9 * kSA * 2) << 16);
+              mma_m16n8k16_bf16(c, af, bf);
+            }
+            const int r0 = mb * 16 + g, n = nb * 8 + 2 * t;
 #pragma unroll
-              for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-#pragma unroll 4
-              for (int k = 0; k < ks; ++k) {
-                const float av = __bfloat162float(sa[k * rp + r]);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                  const int m = mb + kURowGroups * i;
-                  if (m < rows) acc[i] = fmaf(__bfloat162float(sx[m * ks + k]), av, acc[i]);
-                }
-              }
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int m = mb + kURowGroups * i;
-                if (m < rows)
-                  atomicAdd(uacc + (size_t)(m0 + m) * rp + r,
-                            (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
+            for (int h = 0; h < 2; ++h) {
+              const int r = r0 + 8 * h;
+              if (r < rows) {
+                unsigned long long* dst = uacc + (size_t)(m0 + r) * rp + n;
+                atomicAdd(dst, (unsigned long long)__float2ll_rn(c[2 * h] * (float)(1ll << kUFrac)));
+                atomicAdd(dst + 1, (unsigned long long)__float2ll_rn(c[2 * h + 1] * (float)(1ll << kUFrac)));
               }
             }
           }
         }
-        named_bar_sync(3, kUThreads);  // slot free again for the adapter operands
       } else {
         for (int a = 0; a < p.ra; ++a) {
           const int r = 64 * a + (ut & 63);
@@ -386,8 +420,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             float acc[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-#pragma unroll 4
-            for (int k = k0; k < k1; ++k) {
+            for (int k = k0; k < k0 + ks; ++k) {
               const float av = __bfloat162float(p.acat[(size_t)k * rp + r]);
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -398,32 +431,23 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               const int m = mb + kURowGroups * i;
-              if (m < p.M && k1 > k0)
+              if (m < p.M)
                 atomicAdd(uacc + (size_t)m * rp + r,
                           (unsigned long long)__double2ll_rn((double)acc[i] * (double)(1ll << kUFrac)));
             }
           }
         }
       }
-      // the previous adapter launch's buffer (other parity) is idle in this
-      // launch: CTA 0 clears it for the next one
-      if (blockIdx.x == 0) {
-        // the previous user of that buffer may have had another shape: clear
-        // exactly the prefix it recorded as used
-        unsigned long long* other = p.u_acc + (size_t)(par ^ 1u) * kUAccElems;
-        const uint32_t used = p.ctrl[kCtrlUsed + (par ^ 1u)];
-        for (uint32_t i = (uint32_t)ut; i < used; i += kUThreads) other[i] = 0ull;
-        if (ut == 0) {
-          p.ctrl[kCtrlReady + (par ^ 1u)] = 0u;
-          p.ctrl[kCtrlUsed + (par ^ 1u)] = 0u;
-          p.ctrl[kCtrlUsed + par] = (uint32_t)(p.M * rp);
-        }
-      }
-      named_bar_sync(3, kUThreads);
-      if (ut == 0) {
-        __threadfence();
-        atomicAdd(p.ctrl + kCtrlReady + par, 1u);
-      }
+      ++done;
+      if (ut == 0 && done == 1) SALR_TRACE(17);
+      named_bar_sync(3, kUThreads);  // staging area reused by the next slice
+      if (ut == 0 && done == 1) SALR_TRACE(18);
+    }
+    if (ut == 0 && done) {
+      __threadfence();
+      atomicAdd(p.ctrl + kCtrlReady + par, done);  // consumers wait for all slices
+      SALR_TRACE(13);
+    }
   }
 
   if (warp == kWarpProd0 || warp == kWarpProd1) {
@@ -625,8 +649,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (!u_ok) {
           if (etid == 0) {
             const volatile uint32_t* rdy = p.ctrl + kCtrlReady + par;
-            while (*rdy < (uint32_t)G) __nanosleep(128);
+            const uint32_t nsl = (uint32_t)((p.K + kUSlice - 1) / kUSlice);
+            while (*rdy < nsl) __nanosleep(128);
             __threadfence();
+            SALR_TRACE(14);
           }
           named_bar_sync(1, 128);
           u_ok = true;

@@ -115,6 +115,16 @@ __device__ __forceinline__ uint32_t lds_u16(uint32_t saddr) {
   return v;
 }
 
+// Warp-level bf16 MMA m16n8k16 (fp32 accumulate) for the small adapter
+// product U = X A_cat, where a tcgen05 tile would be mostly padding.
+__device__ __forceinline__ void mma_m16n8k16_bf16(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
 // ---------------------------------------------------------------- TMA
 // 1-D bulk copy global -> shared, completion on an mbarrier (complete_tx).
 __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,

@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for m in 3; do
-  echo "######## mode $m"; SALR_DEBUG_MODE=$m timeout 120 python tools/trace_linear.py --shape gate --tokens 1 --no-adapters --launches 2
-done > gpurun_out/trace.txt 2>&1
+for sh in k down; do for m in 1 32; do
+  echo "######## $sh M=$m"; timeout 120 python tools/trace_linear.py --shape $sh --tokens $m --launches 2 --graph
+done; done > gpurun_out/trace.txt 2>&1
 echo done
