@@ -136,6 +136,12 @@ size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pa
  * write per-CTA %globaltimer stamps of pipeline events into buf[cta][32]
  * (u64, device memory, >= 32 * 8 * num_ctas bytes).  NULL disables. */
 int salr_debug_set_trace(void* buf);
+/* Instrumentation (tests/tools): configuration of the most recent
+ * salr_linear_forward launch on this host thread's process: {ctas, stages,
+ * BM, decoder groups, u_mode (0 none, 1 in-kernel U, 2 U pre-kernel), coop,
+ * cluster size (0 = global split-K reduction), pdl, cluster size requested,
+ * max co-resident clusters (-1 = not queried), dynamic smem bytes, 0}. */
+int salr_debug_last_launch(int32_t* info12);
 /* flags: SALR_FLAG_PDL launches the kernel as a programmatic dependent of the
  * preceding work on the stream: its weight-streaming prologue overlaps the
  * tail of that work and it waits for it (griddepcontrol.wait) before reading

@@ -17,6 +17,8 @@ from .errors import (BoundsError, ConfigError, CorruptionError, DomainError, For
                      SalrError, ShapeError)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsalr_b200.so")
+# tools/ab.sh: A/B-compare two builds of the library in one process launch
+LIB_PATH = os.environ.get("SALR_B200_LIB_AB", LIB_PATH)
 
 F32, BF16, F64 = 0, 1, 2
 TILE_K, TILE_N = 64, 128
@@ -40,6 +42,7 @@ _SIGS = {
     "salr_tb2_write": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp], _int),
     "salr_linear_workspace_bytes": ([_i64, _i64, _i64, _i64, _int], ctypes.c_size_t),
     "salr_debug_set_trace": ([_vp], _int),
+    "salr_debug_last_launch": ([_vp], _int),
     "salr_linear_forward": ([_vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _int, _i64,
                              _vp, ctypes.c_size_t, _int, _int, _int, _vp], _int),
 }
@@ -61,6 +64,8 @@ def load() -> ctypes.CDLL:
                                 "(run `python -m paper_2601_16991_b200._build`)")
             lib = ctypes.CDLL(LIB_PATH)
             for name, (args, res) in _SIGS.items():
+                if "SALR_B200_LIB_AB" in os.environ and not hasattr(lib, name):
+                    continue  # an older build under A/B comparison
                 fn = getattr(lib, name)
                 fn.argtypes, fn.restype = args, res
             _lib = lib

@@ -71,6 +71,8 @@ struct LinearParams {
   int y_dtype;
   int stages;         // ring slots in use
   int coop;           // 1: grid <= SM count, split tiles are reduced cooperatively
+  int cluster;        // > 1: every output tile is split over exactly the `cluster`
+                      // CTAs of one thread-block cluster; reduced through DSMEM
   uint32_t rec_slot;  // bytes per ring slot: the largest record of this matrix, 16-aligned
   int dbg;            // timing experiments only: 1 = skip decode, 2 = skip record loads
   unsigned long long* trace;  // optional per-CTA event timestamps (globaltimer ns), [G][32]
@@ -142,6 +144,22 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* addr) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
   return v;
 }
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t saddr, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(saddr), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(ra)
+               : "memory");
+  return v;
+}
+// acquire-release fence at GPU scope (release/acquire patterns with relaxed
+// atomics).  (__threadfence() is the sequentially consistent fence.)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t v) {
   uint32_t old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(addr), "r"(v) : "memory");
@@ -153,7 +171,7 @@ __device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t 
 // each serial role is split across warps that work on different units
 // concurrently: two producers (even / odd units), two row-base warps, and
 // kDecGroups decoder groups (group g decodes units it = g mod kDecGroups).
-constexpr int kWarpProd0 = 0, kWarpMma = 1;  // warps 2-3 idle
+constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPub = 2;  // warp 3 idle
 constexpr int kWarpProd1 = 24;
 
 template <int BM, int kDecGroups>
@@ -186,6 +204,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ad_empty + 1);
   volatile uint32_t* last_flag = tmem_slot + 1;
   uint32_t* zero_word = tmem_slot + 2;  // a shared zero the decoders load for absent elements
+  volatile uint32_t* early_old_slot = tmem_slot + 3;  // publisher warp -> epilogue
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -200,6 +219,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const int u_begin = (int)((int64_t)blockIdx.x * p.units / G);
   const int u_end = (int)(((int64_t)blockIdx.x + 1) * p.units / G);
   const int tiles_per_mc = p.n_nt * p.n_kt;
+  // The CTA's first segment is a split tile with more work behind it: its
+  // partial is published mid-run by the publisher warp (see the epilogue).
+  const int first_seg_end0 = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
+  const bool early_split = !p.cluster && (u_begin % p.n_kt != 0 || first_seg_end0 - u_begin < p.n_kt) &&
+                           first_seg_end0 < u_end;
 
   // ---- producer state (warps kWarpProd0 / kWarpProd1, units of one parity).
   // Record offsets are fetched 32 units at a time, one chunk ahead, one
@@ -300,6 +324,43 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       for (int v = pv0; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
     __syncwarp();
   }
+  // ---- in-kernel U (u_mode 1) geometry.  K is cut into slices of kUSlice
+  // rows.  CTA c owns slice c; slices >= G are claimed dynamically.  A_cat is
+  // a weight, so the A rows of the owned slice are copied into the (still
+  // unused) adapter slot before waiting for the preceding kernel, and the
+  // dynamically claimed ones are prefetched into L2.  (Everything U-related
+  // is recomputed where used: nothing stays live across the decode loops.)
+  constexpr int kSX = kUSlice + 8;  // X chunk row stride (pads: conflict-free
+  auto u_geom_wide = [&]() { return (p.dbg & 4) ? false : ((u_end - u_begin) < 24 && p.M >= 16); };
+  auto u_kSA = [&]() { return 64 * p.ra + 8; };  // A slice row stride   mma fragment loads)
+  auto u_staged_fn = [&]() {
+    return (p.K % 8 == 0) &&
+           (uint32_t)(kUSlice * u_kSA() + BM * kSX) * 2u <= (uint32_t)p.ra * (kAdTileBytes + 2u * BM * 128u);
+  };
+  // stage A rows of slice sl (zero rows past K, up to a whole mma k-step)
+  auto u_load_a = [&](int sl, int ut, int nthr) {
+    const int rp = 64 * p.ra, kSA = u_kSA();
+    __nv_bfloat16* const sa = reinterpret_cast<__nv_bfloat16*>(adbuf);
+    const int k0 = sl * kUSlice, ks = min(kUSlice, p.K - k0), ks16 = (ks + 15) & ~15;
+    const int cpr = rp / 8;  // 16-byte chunks per row
+    const __nv_bfloat16* src = p.acat + (size_t)k0 * rp;
+    for (int i = ut; i < ks16 * cpr; i += nthr) {
+      const int kr = i / cpr, c = i % cpr;
+      cp_async_16(smem_u32(sa + kr * kSA + 8 * c), src + (size_t)(kr < ks ? i : 0) * 8, kr < ks ? 16u : 0u);
+    }
+  };
+  if (p.u_mode == 1) {
+    const bool wide = u_geom_wide();
+    if (warp >= (wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4 && u_staged_fn()) {
+      const int ut = (warp - (wide ? kFirstDecWarp : kFirstEpiWarp)) * 32 + (int)lane;
+      const int nsl = (p.K + kUSlice - 1) / kUSlice;
+      if ((int)blockIdx.x < nsl) u_load_a((int)blockIdx.x, ut, wide ? 640 : 128);
+      const int pf = G + (int)blockIdx.x;  // a slice another CTA may claim
+      if (ut == 0 && pf < nsl)
+        prefetch_l2_bulk(p.acat + (size_t)pf * kUSlice * 64 * p.ra,
+                         (uint32_t)(min(kUSlice, p.K - pf * kUSlice) * 64 * p.ra * 2));
+    }
+  }
   if (warp == kWarpMma) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
@@ -308,20 +369,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (threadIdx.x == 0) SALR_TRACE(0);
   const uint32_t a_col0 = (uint32_t)((NACC * ACOLS + 31) & ~31);  // first A-stage column
 
-  // ---- in-kernel U = X @ A_cat (u_mode 1).  K is cut into slices of
-  // kUSlice rows that CTAs claim dynamically (atomic counter): CTAs that
-  // start early (programmatic launches start staggered) do the work, late
-  // ones find none left, so U is ready soon after the first CTAs start.
-  // Each slice partial goes into the int64 fixed-point accumulator (integer
-  // atomics: order-independent, bit-reproducible).  Participants: the
-  // epilogue warps, plus the decoder warps for short launches with M >= 16
-  // (work-bound partials); with few tokens it is latency-bound.
-  const bool u_wide = (p.dbg & 4) ? false : ((u_end - u_begin) < 24 && p.M >= 16);
+  // ---- in-kernel U = X @ A_cat (u_mode 1): each slice partial goes into
+  // the int64 fixed-point accumulator (integer atomics: order-independent,
+  // bit-reproducible) and is published at once (slices-done counter).
+  // Participants: the epilogue warps, plus the decoder warps for short
+  // launches with M >= 16 (work-bound partials); with few tokens it is
+  // latency-bound.
+  const bool u_wide = u_geom_wide();
   const int kUThreads = u_wide ? 640 : 128;
-  const int kURowGroups = kUThreads / 64;
   if (p.u_mode == 1 && warp >= (u_wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4) {
     const int ut = (warp - (u_wide ? kFirstDecWarp : kFirstEpiWarp)) * 32 + (int)lane;
     const int rp = 64 * p.ra;
+    const int kSA = u_kSA();
     pdl_wait();  // X may be the preceding kernel's output
     const uint32_t par = *reinterpret_cast<volatile uint32_t*>(p.ctrl + kCtrlEpoch) & 1u;
     unsigned long long* uacc = p.u_acc + (size_t)par * kUAccElems;
@@ -340,35 +399,20 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
     }
     const int nsl = (p.K + kUSlice - 1) / kUSlice;
-    // staged slices: A slice (kUSlice x rp, row stride rp+8) and an X row
-    // chunk (BM x kUSlice, row stride kUSlice+8; the pads make the mma
-    // fragment loads bank-conflict free) in the still unused adapter slot.
-    constexpr int kSX = kUSlice + 8;
-    const int kSA = rp + 8;
-    const uint32_t slot_bytes = (uint32_t)p.ra * (kAdTileBytes + 2u * BM * 128u);
-    const bool staged = (p.K % 8 == 0) && (uint32_t)(kUSlice * kSA + BM * kSX) * 2u <= slot_bytes;
+    const bool staged = u_staged_fn();
     __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(adbuf);
     __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(adbuf + (uint32_t)kUSlice * kSA * 2u);
+    const int kURowGroups = kUThreads / 64;
     const int rg = ut >> 6;  // row group 0..kURowGroups-1 (scalar path)
     uint32_t done = 0;
+    int sl = (int)blockIdx.x;  // owned slice (A rows already in flight)
     for (;;) {
-      if (ut == 0) *last_flag = atomicAdd(p.ctrl + kCtrlSlice + par, 1u);
-      named_bar_sync(3, kUThreads);
-      const int sl = (int)*last_flag;
-      named_bar_sync(3, kUThreads);
       if (ut == 0 && done == 0) SALR_TRACE(15);
       if (sl >= nsl) break;
       const int k0 = sl * kUSlice, ks = min(kUSlice, p.K - k0);
       if (staged) {
         const int ks16 = (ks + 15) & ~15;  // zero-padded to whole mma k-steps
-        {  // A slice rows k0..k0+ks are contiguous in A_cat
-          const uint4* src = reinterpret_cast<const uint4*>(p.acat + (size_t)k0 * rp);
-          const int cpr = rp / 8;  // 16-byte chunks per row
-          for (int i = ut; i < ks16 * cpr; i += kUThreads) {
-            const int kr = i / cpr, c = i % cpr;
-            reinterpret_cast<uint4*>(sa + kr * kSA)[c] = kr < ks ? __ldg(src + i) : make_uint4(0u, 0u, 0u, 0u);
-          }
-        }
+        if (done > 0) u_load_a(sl, ut, kUThreads);
         const int wid = ut >> 5, nw = kUThreads / 32;
         const int g = (int)lane >> 2, t = (int)lane & 3;
         const uint32_t sa_u = smem_u32(sa), sx_u = smem_u32(sx);
@@ -377,10 +421,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           if (m0) named_bar_sync(3, kUThreads);  // previous chunk consumed
           for (int i = ut; i < rows * (ks16 / 8); i += kUThreads) {
             const int m = i / (ks16 / 8), c = i % (ks16 / 8);
-            reinterpret_cast<uint4*>(sx + m * kSX)[c] =
-                c < ks / 8 ? __ldg(reinterpret_cast<const uint4*>(p.x + (size_t)(m0 + m) * p.ldx + k0) + c)
-                           : make_uint4(0u, 0u, 0u, 0u);
+            cp_async_16(smem_u32(sx + m * kSX + 8 * c),
+                        p.x + (size_t)(m0 + m) * p.ldx + k0 + (c < ks / 8 ? 8 * c : 0), c < ks / 8 ? 16u : 0u);
           }
+          cp_async_wait_all();
           named_bar_sync(3, kUThreads);
           if (ut == 0 && done == 0 && m0 == 0) SALR_TRACE(16);
           // (16-row block, 8-column block) items over the warps; rows past
@@ -389,16 +433,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           for (int it = wid; it < items; it += nw) {
             const int nb = it % nnb, mb = it / nnb;
             float c[4] = {0.f, 0.f, 0.f, 0.f};
+            // fragments by ldmatrix: X rows (lane & 15) at k + 8 (lane >> 4);
+            // A_cat k rows (lane & 15), transposed into the col-major B operand
+            const uint32_t xa = sx_u + (uint32_t)(((mb * 16 + (int)(lane & 15)) * kSX + 8 * (int)(lane >> 4)) * 2);
+            const uint32_t aa = sa_u + (uint32_t)(((int)(lane & 15) * kSA + nb * 8) * 2);
             for (int kk = 0; kk < ks16; kk += 16) {
               uint32_t af[4], bf[2];
-              const uint32_t xa = sx_u + (uint32_t)(((mb * 16 + g) * kSX + kk + 2 * t) * 2);
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(af[0]) : "r"(xa));
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(af[1]) : "r"(xa + 8 * kSX * 2));
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(af[2]) : "r"(xa + 16));
-              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(af[3]) : "r"(xa + 8 * kSX * 2 + 16));
-              const uint32_t aa = sa_u + (uint32_t)(((kk + 2 * t) * kSA + nb * 8 + g) * 2);
-              bf[0] = lds_u16(aa) | (lds_u16(aa + kSA * 2) << 16);
-              bf[1] = lds_u16(aa + 8 * kSA * 2) | (lds_u16(aa + 9 * kSA * 2) << 16);
+              asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(af[0]), "=r"(af[1]), "=r"(af[2]), "=r"(af[3])
+                           : "r"(xa + (uint32_t)kk * 2));
+              asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                           : "=r"(bf[0]), "=r"(bf[1])
+                           : "r"(aa + (uint32_t)kk * kSA * 2));
               mma_m16n8k16_bf16(c, af, bf);
             }
             const int r0 = mb * 16 + g, n = nb * 8 + 2 * t;
@@ -440,14 +486,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
       ++done;
       if (ut == 0 && done == 1) SALR_TRACE(17);
-      named_bar_sync(3, kUThreads);  // staging area reused by the next slice
-      if (ut == 0 && done == 1) SALR_TRACE(18);
+      named_bar_sync(3, kUThreads);  // every partial of this slice issued; staging reusable
+      if (ut == 0) {
+        fence_acq_rel_gpu();
+        atomicAdd(p.ctrl + kCtrlReady + par, 1u);  // consumers wait for all slices
+        if (done == 1) SALR_TRACE(18);
+        // next slice: dynamic claims hand out slices G, G+1, ...
+        *last_flag = (uint32_t)G + atomicAdd(p.ctrl + kCtrlSlice + par, 1u);
+      }
+      named_bar_sync(3, kUThreads);
+      sl = (int)*last_flag;
+      named_bar_sync(3, kUThreads);
     }
-    if (ut == 0 && done) {
-      __threadfence();
-      atomicAdd(p.ctrl + kCtrlReady + par, done);  // consumers wait for all slices
-      SALR_TRACE(13);
-    }
+    if (ut == 0 && done) SALR_TRACE(13);
   }
 
   if (warp == kWarpProd0 || warp == kWarpProd1) {
@@ -456,6 +507,22 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (producer)
       while (pv < u_end) issue_one(true);
     if (lane == 0 && pk == 0) SALR_TRACE(2);
+  } else if (warp == kWarpPub) {
+    // ================= publisher: releases the first split partial at GPU
+    // scope (fence + ticket) so the epilogue warps never stall on it
+    if (early_split) {
+      named_bar_sync(5, 160);  // epilogue: partial stored (bar.arrive)
+      if (lane == 0) {
+        const int tb = u_begin - u_begin % p.n_kt;
+        fence_acq_rel_gpu();  // release (barrier + cumulativity)
+        const uint32_t old = atomicAdd(&p.tickets[(tb / tiles_per_mc) * p.n_nt + (tb / p.n_kt) % p.n_nt], 1u);
+        const int np = cta_of(tb + p.n_kt - 1, p.units, G) - cta_of(tb, p.units, G) + 1;
+        if (!p.coop && old + 1 == (uint32_t)np) fence_acq_rel_gpu();  // we reduce it: acquire
+        *early_old_slot = old;
+      }
+      __syncwarp();
+      named_bar_arrive(6, 160);
+    }
   } else if (warp == kWarpMma) {
     // ================= MMA issuer: the whole warp walks the schedule (warp-
     // uniform state stays in uniform registers); one elected lane issues.
@@ -648,10 +715,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       if (p.u_mode == 1) {
         if (!u_ok) {
           if (etid == 0) {
-            const volatile uint32_t* rdy = p.ctrl + kCtrlReady + par;
-            const uint32_t nsl = (uint32_t)((p.K + kUSlice - 1) / kUSlice);
-            while (*rdy < nsl) __nanosleep(128);
-            __threadfence();
+            // acquire pairs with the producers' fence + counter increment
+            while (ld_acquire_u32(p.ctrl + kCtrlReady + par) < (uint32_t)((p.K + kUSlice - 1) / kUSlice))
+              __nanosleep(32);
             SALR_TRACE(14);
           }
           named_bar_sync(1, 128);
@@ -710,44 +776,78 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // Sum the partial tiles of a split output tile (the unit range starting
     // at tile_base) over CTAs c_first..c_last in that fixed order
     // (deterministic); this CTA takes share `share` of `nshare` row slices.
-    auto reduce_split = [&](int tile_base, int share, int nshare, bool reset) {
+    auto reduce_split = [&](int tile_base, int share, int nshare, bool reset, int t0, int nthr) {
       const int nt = (tile_base / p.n_kt) % p.n_nt;
       const int mc = tile_base / (p.n_kt * p.n_nt);
       const int rows = min(BM, p.M - mc * BM);
       const int c_first = cta_of(tile_base, p.units, G), c_last = cta_of(tile_base + p.n_kt - 1, p.units, G);
-      const int n2 = nt * kTileN + etid;
       // CTA c > c_first begins inside this tile (its slot 0); c_first
       // holds it in slot 1 unless its range starts exactly at the tile.
       const int cb_first = (int)((int64_t)c_first * p.units / G);
       const size_t tile_elems = (size_t)BM * kTileN;
-      const float* p_first =
-          p.partials + ((size_t)c_first * 2 + (cb_first >= tile_base ? 0 : 1)) * tile_elems + etid;
-      const float* p_rest = p.partials + etid;  // + (2 c) * tile_elems
+      const float* p_first = p.partials + ((size_t)c_first * 2 + (cb_first >= tile_base ? 0 : 1)) * tile_elems;
       const int r0 = share * rows / nshare, r1 = (share + 1) * rows / nshare;
-      for (int m0 = r0; m0 < r1; m0 += 8) {
-        float acc[8];
+      auto store_y = [&](size_t o, int col, float v) {
+        if (col >= p.N) return;
+        if (p.y_dtype == kF32) static_cast<float*>(p.y)[o] = v;
+        else static_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(v);
+      };
+      if (r1 - r0 <= 2) {
+        // few rows (decode-size M): one element per thread and pass, up to
+        // 16 partials in flight -- a single round trip for most tiles
+        for (int e = etid - t0; e < (r1 - r0) * kTileN; e += nthr) {
+          const int m = r0 + e / kTileN, cl = e % kTileN;
+          const size_t off = (size_t)m * kTileN + cl;
+          float acc = __ldcg(p_first + off);
+          for (int c = c_first + 1; c <= c_last; c += 8) {
+            float v[8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
-          acc[i] = (m0 + i < r1) ? __ldcg(p_first + (size_t)(m0 + i) * kTileN) : 0.0f;
-#pragma unroll 4
-        for (int c = c_first + 1; c <= c_last; ++c) {
-          const float* pt = p_rest + (size_t)c * 2 * tile_elems + (size_t)m0 * kTileN;
+            for (int i = 0; i < 8; ++i)
+              if (c + i <= c_last) v[i] = __ldcg(p.partials + (size_t)(c + i) * 2 * tile_elems + off);
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            if (m0 + i < r1) acc[i] += __ldcg(pt + (size_t)i * kTileN);
-        }
-        if (n2 < p.N) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (m0 + i >= r1) break;
-            const size_t o = (size_t)(mc * BM + m0 + i) * p.ldy + n2;
-            if (p.y_dtype == kF32) static_cast<float*>(p.y)[o] = acc[i];
-            else static_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(acc[i]);
+            for (int i = 0; i < 8; ++i)
+              if (c + i <= c_last) acc += v[i];
           }
+          store_y((size_t)(mc * BM + m) * p.ldy + nt * kTileN + cl, nt * kTileN + cl, acc);
+        }
+      } else {
+        // one 4-column chunk per thread and pass; the partials of a chunk are
+        // loaded in batches of 8 independent 16-byte loads
+        for (int e = etid - t0; e < (r1 - r0) * (kTileN / 4); e += nthr) {
+          const int m = r0 + e / (kTileN / 4), c4 = 4 * (e % (kTileN / 4));
+          const size_t off = (size_t)m * kTileN + c4;
+          float4 acc = __ldcg(reinterpret_cast<const float4*>(p_first + off));
+          for (int c = c_first + 1; c <= c_last; c += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (c + i <= c_last)
+                v[i] = __ldcg(reinterpret_cast<const float4*>(p.partials + (size_t)(c + i) * 2 * tile_elems + off));
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (c + i <= c_last) {
+                acc.x += v[i].x;
+                acc.y += v[i].y;
+                acc.z += v[i].z;
+                acc.w += v[i].w;
+              }
+          }
+          const size_t o = (size_t)(mc * BM + m) * p.ldy + nt * kTileN + c4;
+          store_y(o, nt * kTileN + c4, acc.x);
+          store_y(o + 1, nt * kTileN + c4 + 1, acc.y);
+          store_y(o + 2, nt * kTileN + c4 + 2, acc.z);
+          store_y(o + 3, nt * kTileN + c4 + 3, acc.w);
         }
       }
-      if (reset && etid == 0) p.tickets[mc * p.n_nt + nt] = 0u;
+      if (reset && etid == t0) p.tickets[mc * p.n_nt + nt] = 0u;
     };
+    auto tile_np = [&](int tb) {
+      return cta_of(tb + p.n_kt - 1, p.units, G) - cta_of(tb, p.units, G) + 1;
+    };
+    auto tile_ticket = [&](int tb) {
+      return &p.tickets[(tb / (p.n_kt * p.n_nt)) * p.n_nt + (tb / p.n_kt) % p.n_nt];
+    };
+    bool early_pub = false;  // first split segment already published in the loop
     int seg = 0;
     int u = u_begin;
     while (u < u_end) {
@@ -768,25 +868,45 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int n = nt * kTileN + nl;
       const bool n_ok = n < p.N;
       const int rows = min(BM, p.M - mc * BM);
+      if (etid == 0) SALR_TRACE_UNIT(12, seg);
+      // Drain the accumulator 16 rows at a time (two loads in flight).  The
+      // destination mode is uniform per segment, so each mode gets its own
+      // branch-free store loop:
+      //   full tile      -> y (row-major, lanes along n: coalesced)
+      //   cluster split  -> own smem, n-major [128][BM+4] (16-byte stores,
+      //                     conflict-free), reduced through DSMEM at the end
+      //   global split   -> partial slot [BM][128] (coalesced)
+      const int mode = full_cover ? (p.y_dtype == kF32 ? 0 : 1) : (p.cluster ? 2 : 3);
+      float* const sp_col = reinterpret_cast<float*>(xbuf) + nl * (BM + 4);
+      const size_t yrow0 = (size_t)(mc * BM) * p.ldy + n;
 #pragma unroll 1
       for (int c0 = 0; c0 < rows; c0 += 8) {
         uint32_t r[8];
         SALR_TMEM_LD_X8(tmem + lane_tm + (uint32_t)(b * ACOLS + c0), r);
         tc_wait_ld();
+        if (mode == 2) {
+          *reinterpret_cast<uint4*>(sp_col + c0) = make_uint4(r[0], r[1], r[2], r[3]);
+          *reinterpret_cast<uint4*>(sp_col + c0 + 4) = make_uint4(r[4], r[5], r[6], r[7]);
+        } else if (mode == 3) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (c0 + i >= rows) break;
-          const float val = __uint_as_float(r[i]);
-          if (full_cover) {
-            if (!n_ok) continue;
-            const size_t o = (size_t)(mc * BM + c0 + i) * p.ldy + n;
-            if (p.y_dtype == kF32) static_cast<float*>(p.y)[o] = val;
-            else static_cast<__nv_bfloat16*>(p.y)[o] = __float2bfloat16_rn(val);
+          for (int i = 0; i < 8; ++i)
+            if (c0 + i < rows) __stcg(part_tile + (size_t)(c0 + i) * kTileN + nl, __uint_as_float(r[i]));
+        } else if (n_ok) {
+          if (mode == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (c0 + i < rows) static_cast<float*>(p.y)[yrow0 + (size_t)(c0 + i) * p.ldy] = __uint_as_float(r[i]);
           } else {
-            __stcg(part_tile + (size_t)(c0 + i) * kTileN + nl, val);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              if (c0 + i < rows)
+                static_cast<__nv_bfloat16*>(p.y)[yrow0 + (size_t)(c0 + i) * p.ldy] =
+                    __float2bfloat16_rn(__uint_as_float(r[i]));
           }
         }
       }
+      if (etid == 0 && seg == 0) SALR_TRACE(25);
+      if (etid == 0) SALR_TRACE_UNIT(14, seg);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[b]);
@@ -796,52 +916,90 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         prep_adapter(next_ad);
         next_ad = next_first_k(next_ad + 1);
       }
-
-      if (!full_cover) {
-        // publish this CTA's partial of a split output tile (no waiting here:
-        // the reduction runs after the CTA's last segment, see below)
-        named_bar_sync(1, 128);  // all 128 partial columns stored (CTA scope)
-        if (etid == 0) {
-          const int c_first = cta_of(tile_base, p.units, G), c_last = cta_of(tile_base + p.n_kt - 1, p.units, G);
-          // acq_rel at GPU scope publishes this CTA's partial (ordered before
-          // by the CTA barrier + cumulativity) and acquires the others'.
-          const uint32_t old = ticket_add_acq_rel(&p.tickets[mc * p.n_nt + nt], 1u);
-          if (!p.coop) *last_flag = (old + 1 == (uint32_t)(c_last - c_first + 1)) ? 1u : 0u;
-        }
-        named_bar_sync(1, 128);
-        if (!p.coop && *last_flag) reduce_split(tile_base, 0, 1, true);
-        named_bar_sync(1, 128);
+      if (!full_cover && !p.cluster && seg_end < u_end) {
+        // (== early_split: only the first segment can be split and followed)
+        // a split segment with more work behind it (only the CTA's first
+        // segment can be one): publish its partial now, off the critical
+        // path.  (Its last-CTA reduction, if ours -- rare: the CTA before us
+        // finishes its part of this tile last -- waits for the tail below.)
+        named_bar_arrive(5, 160);  // hand the stored partial to the publisher warp
+        early_pub = true;
       }
+
       ++seg;
       u = seg_end;
     }
-    if (p.coop && u_begin < u_end) {
-      // Cooperative reduction of this CTA's split tiles (at most its first
-      // and its last segment), after all of its own partials are out: wait
-      // until every participant has published, then reduce our row share.
-      const int tiles[2] = {u_begin - u_begin % p.n_kt, (u_end - 1) - (u_end - 1) % p.n_kt};
-      for (int j = 0; j < 2; ++j) {
-        const int tb = tiles[j];
-        if (j == 1 && tb == tiles[0]) break;
-        const bool split = !(u_begin <= tb && tb + p.n_kt <= u_end);
-        if (!split) continue;
-        const int c_first = cta_of(tb, p.units, G), c_last = cta_of(tb + p.n_kt - 1, p.units, G);
-        const int np = c_last - c_first + 1;
-        const int nt = (tb / p.n_kt) % p.n_nt, mc = tb / (p.n_kt * p.n_nt);
-        uint32_t* tk = &p.tickets[mc * p.n_nt + nt];
-        if (etid == 0)
-          while (ld_acquire_u32(tk) < (uint32_t)np) __nanosleep(64);
-        named_bar_sync(1, 128);
-        reduce_split(tb, (int)blockIdx.x - c_first, np, false);
-        named_bar_sync(1, 128);
-        if (etid == 0) {
-          // the last participant out resets both counters for the next launch
-          uint32_t* dn = tk + kDoneTicketOff;
-          if (atomicAdd(dn, 1u) + 1 == (uint32_t)np) {
-            *tk = 0u;
-            *dn = 0u;
+    // ---- split-K tail (global path).  A CTA shares at most two output tiles
+    // (its first and its last segment).  The first was published in the loop
+    // if work followed it; publish the rest with one release and relaxed
+    // ticket increments issued back to back (round trips overlap), then
+    //   coop (M >= 16): wait for every participant, reduce our row share, or
+    //   last-CTA:       the CTA completing a ticket reduces the whole tile.
+    // The in-kernel U epoch ticket rides along: this CTA is done with U.
+    int tl[2];
+    int nsplit = 0;
+    if (!p.cluster && u_begin < u_end) {
+      const int t0 = u_begin - u_begin % p.n_kt, t1 = (u_end - 1) - (u_end - 1) % p.n_kt;
+      if (!(t0 >= u_begin && t0 + p.n_kt <= u_end)) tl[nsplit++] = t0;
+      if (t1 != t0 && !(t1 >= u_begin && t1 + p.n_kt <= u_end)) tl[nsplit++] = t1;
+    }
+    // tiles still to publish: all but the early-published first one
+    const int jpub = early_pub ? 1 : 0;
+    if (nsplit > jpub) named_bar_sync(1, 128);  // every partial of this CTA stored (CTA scope)
+    if (early_pub) named_bar_sync(6, 160);  // the publisher's ticket value is in
+    if (etid == 0 && (nsplit || p.u_mode == 1)) {
+      SALR_TRACE(29);
+      uint32_t old[2] = {early_pub ? *early_old_slot : 0u, 0u};
+      // acq_rel: publishes the last partial and acquires the others' (and
+      // orders this CTA's U reads before the epoch ticket below)
+      if (nsplit > jpub) old[nsplit - 1] = ticket_add_acq_rel(tile_ticket(tl[nsplit - 1]), 1u);
+      else if (p.u_mode == 1) fence_acq_rel_gpu();
+      uint32_t lf = 0;
+#pragma unroll
+      for (int j = 0; j < nsplit; ++j)
+        if (!p.coop && old[j] + 1 == (uint32_t)tile_np(tl[j])) lf |= 1u << j;
+      if (p.u_mode == 1) {
+        // this CTA's U slices are published and its U reads done; the last
+        // CTA advances the epoch (flips the U parity) for the next launch on
+        // this workspace
+        const uint32_t d = atomicAdd(p.ctrl + kCtrlDone, 1u);
+        if (d + 1 == (uint32_t)G) {
+          p.ctrl[kCtrlDone] = 0u;
+          fence_acq_rel_gpu();
+          p.ctrl[kCtrlEpoch] = p.ctrl[kCtrlEpoch] + 1u;
+        }
+      }
+      *last_flag = lf;
+      SALR_TRACE(30);
+    }
+    if (nsplit) {
+      named_bar_sync(1, 128);
+      if (p.coop) {
+        // wait for every participant of a tile, reduce our row share
+#pragma unroll
+        for (int j = 0; j < nsplit; ++j) {
+          const int tb = tl[j], np = tile_np(tb);
+          uint32_t* tk = tile_ticket(tb);
+          if (etid == 0)
+            while (ld_acquire_u32(tk) < (uint32_t)np) __nanosleep(32);
+          named_bar_sync(1, 128);
+          reduce_split(tb, (int)blockIdx.x - cta_of(tb, p.units, G), np, false, 0, 128);
+          named_bar_sync(1, 128);
+          if (etid == 0) {
+            SALR_TRACE(22);
+            // the last participant out resets both counters for the next launch
+            if (atomicAdd(tk + kDoneTicketOff, 1u) + 1 == (uint32_t)np) {
+              tk[0] = 0u;
+              tk[kDoneTicketOff] = 0u;
+            }
           }
         }
+      } else {
+        const uint32_t lf = *last_flag;
+#pragma unroll
+        for (int j = 0; j < nsplit; ++j)
+          if ((lf >> j) & 1u) reduce_split(tl[j], 0, 1, true, 0, 128);
+        if (etid == 0 && lf) SALR_TRACE(31);
       }
     }
     if (etid == 0) SALR_TRACE(8);
@@ -849,20 +1007,53 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) SALR_TRACE(26);
   if (warp == kWarpMma) {
     tc_fence_after();
-    if (lane == 0) SALR_TRACE(9);
     tmem_dealloc(tmem, 512);
   }
-  if (p.u_mode == 1 && threadIdx.x == 0) {
-    // the last CTA of this launch advances the epoch (flips the U parity)
-    const uint32_t old = ticket_add_acq_rel(p.ctrl + kCtrlDone, 1u);
-    if (old + 1 == (uint32_t)G) {
-      p.ctrl[kCtrlDone] = 0u;
-      __threadfence();
-      p.ctrl[kCtrlEpoch] = p.ctrl[kCtrlEpoch] + 1u;
+  if (p.cluster) {
+    // split-K reduction of this cluster's output tile through distributed
+    // shared memory: CTA rank j sums rows [j, j+1) * rows / np of the np
+    // partials in rank (= k) order -- the same order as the global path.
+    cluster_sync_all();  // every partial of the cluster is in shared memory
+    if (threadIdx.x == 0) SALR_TRACE(27);
+    const int np = p.cluster;
+    const int rank = (int)(blockIdx.x % (unsigned)np);
+    const int tb = u_begin - u_begin % p.n_kt;
+    const int nt = (tb / p.n_kt) % p.n_nt, mc = tb / (p.n_kt * p.n_nt);
+    const int rows = min(BM, p.M - mc * BM);
+    // groups of 4 rows: CTA rank j owns groups [j, j+1) * ng / np
+    const int ng = (rows + 3) / 4;
+    const int g0 = rank * ng / np, g1 = (rank + 1) * ng / np;
+    const uint32_t sp = smem_u32(xbuf);
+    for (int e = threadIdx.x; e < (g1 - g0) * kTileN; e += kNumThreads) {
+      const int nl = e % kTileN, m = 4 * (g0 + e / kTileN);
+      const uint32_t a = sp + (uint32_t)((nl * (BM + 4) + m) * 4);
+      float4 acc = ld_dsmem_f4(a, 0u);
+      for (int j = 1; j < np; ++j) {
+        const float4 v = ld_dsmem_f4(a, (uint32_t)j);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      const int n = nt * kTileN + nl;
+      if (n < p.N) {
+        const float o4[4] = {acc.x, acc.y, acc.z, acc.w};
+        const size_t o = (size_t)(mc * BM + m) * p.ldy + n;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (m + i >= rows) break;
+          if (p.y_dtype == kF32) static_cast<float*>(p.y)[o + (size_t)i * p.ldy] = o4[i];
+          else static_cast<__nv_bfloat16*>(p.y)[o + (size_t)i * p.ldy] = __float2bfloat16_rn(o4[i]);
+        }
+      }
     }
+    if (threadIdx.x == 0) SALR_TRACE(28);
+    cluster_sync_all();  // no CTA leaves while its partial is being read
   }
+  if (threadIdx.x == 0) SALR_TRACE(9);
 }
 
 // U[m, r] = sum_k X[m, k] * A_cat[k, r] (fp32), written as bf16 hi + lo
@@ -914,13 +1105,13 @@ __global__ void __launch_bounds__(256) adapter_u_kernel(const __nv_bfloat16* __r
   float* part = u_part + (size_t)blockIdx.y * M * r_pad;
   if (va) __stcg(part + ma * r_pad + r, acc0);
   if (vb) __stcg(part + mb * r_pad + r, acc1);
-  __threadfence();
+  fence_acq_rel_gpu();
   __syncthreads();
   uint32_t* ticket = u_tickets + (size_t)blockIdx.x * gridDim.z + blockIdx.z;
   if (threadIdx.x == 0 && ty == 0) is_last = (atomicAdd(ticket, 1u) + 1 == gridDim.y) ? 1u : 0u;
   __syncthreads();
   if (!is_last) return;
-  __threadfence();
+  fence_acq_rel_gpu();
   for (int j = 0; j < 2; ++j) {
     const int64_t m = j ? mb : ma;
     if (m >= M) continue;
@@ -1000,6 +1191,9 @@ static int max_stages(int bm, int ra, uint32_t rec_slot) {
   return s;
 }
 
+// configuration of the most recent linear launch (salr_debug_last_launch)
+static int g_last_launch[12] = {};
+
 template <int BM, int NG>
 static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cudaStream_t s, bool pdl) {
   auto kern = salr_linear_kernel<BM, NG>;
@@ -1019,12 +1213,51 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   cfg.blockDim = dim3(kNumThreads);
   cfg.dynamicSmemBytes = plan.total;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (p.cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)p.cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = (unsigned)na;
+  const int cluster_req = p.cluster;
+  int cluster_max = -1;
+  if (p.cluster > 1) {
+    // every cluster must be resident at once (else fall back to the global
+    // split-K path); cached per configuration
+    static int64_t cached_key = -1, cached_max = 0;
+    const int64_t key = ((int64_t)p.cluster << 32) | plan.total;
+    if (key != cached_key) {
+      int n = 0;
+      cudaLaunchConfig_t q = cfg;
+      q.attrs = attr + (pdl ? 1 : 0);
+      q.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess) {
+        (void)cudaGetLastError();
+        n = 0;
+      }
+      cached_key = key;
+      cached_max = n;
+    }
+    cluster_max = (int)cached_max;
+    if (cached_max * p.cluster < ctas) {
+      p.cluster = 0;
+      cfg.numAttrs = (unsigned)(na - 1);
+    }
+  }
   SALR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p));
+  const int info[12] = {ctas, p.stages, BM, NG, p.u_mode, p.coop, p.cluster, pdl ? 1 : 0,
+                        cluster_req, cluster_max, (int)plan.total, 0};
+  for (int i = 0; i < 12; ++i) g_last_launch[i] = info[i];
   return SALR_OK;
 }
 
@@ -1103,6 +1336,12 @@ extern "C" {
 // per-CTA globaltimer stamps into buf[G][32] (u64).  NULL disables.
 int salr_debug_set_trace(void* buf) {
   g_trace = static_cast<unsigned long long*>(buf);
+  return SALR_OK;
+}
+
+int salr_debug_last_launch(int32_t* info12) {
+  if (!info12) return SALR_ERR_CONFIG;
+  for (int i = 0; i < 12; ++i) info12[i] = g_last_launch[i];
   return SALR_OK;
 }
 
@@ -1210,6 +1449,16 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   // cooperative split-tile reduction pays off once a partial tile has rows
   // to share (M >= 16); tiny ones stay with the last CTA (one round trip)
   p.coop = (ctas <= sm_count() && M >= 16) ? 1 : 0;
+  {
+    // Split tiles shared by exactly np (2..8) consecutive CTAs: make those a
+    // thread-block cluster and reduce through DSMEM (no global round trips).
+    // The partial tile (BM x 128 fp32) reuses the drained ring.
+    const int64_t per = p.units / ctas;
+    const int64_t np = (p.units % ctas == 0 && per < p.n_kt && p.n_kt % per == 0) ? p.n_kt / per : 0;
+    const bool fits = (int64_t)p.stages * (bm * 128 + p.rec_slot) >= (int64_t)(bm + 4) * kTileN * 4;
+    static const bool no_cluster = getenv("SALR_NO_CLUSTER") != nullptr;
+    p.cluster = (!no_cluster && np >= 2 && np <= 8 && ctas % np == 0 && fits) ? (int)np : 0;
+  }
   p.K = (int)K;
   p.x = static_cast<const __nv_bfloat16*>(x);
   p.acat = static_cast<const __nv_bfloat16*>(acat);

@@ -153,3 +153,43 @@ def test_llama_shapes(S, name, M):
     s = S.encode(li.w_hat, value_dtype="bf16")
     y = S.pipelined_forward(x, s, fused, S.PipelineConfig())
     assert_close(y.cpu().numpy(), _dense_ref(x, li.w_hat, fused).cpu().numpy(), f"{name} M={M}")
+
+
+def _last_launch():
+    import ctypes
+    from paper_2601_16991_b200 import _lib
+    info = (ctypes.c_int32 * 12)()
+    assert _lib.load().salr_debug_last_launch(ctypes.addressof(info)) == 0
+    keys = ("ctas", "stages", "bm", "groups", "u_mode", "coop", "cluster", "pdl", "cluster_req", "cluster_max",
+            "smem")
+    return dict(zip(keys, list(info)))
+
+
+@pytest.mark.parametrize("M", [16, 32, 100])
+@pytest.mark.parametrize("adapters", [False, True])
+def test_split_k_reduction_modes(S, M, adapters):
+    """The three split-K reductions give the same answer: DSMEM within a
+    thread-block cluster (tiles split over exactly np CTAs of one cluster),
+    cooperative global, last-CTA global.  K=4096 (64 k-tiles) x 4096 columns:
+    128 CTAs x 16 units -> clusters of 4."""
+    g = torch.Generator().manual_seed(77 + M)
+    K, N = 4096, 4096
+    w = (torch.randn(K, N, generator=g) * 0.02).bfloat16().float()
+    w[torch.rand(K, N, generator=g) < 0.5] = 0
+    x = torch.randn(M, K, generator=g).bfloat16().float().cuda()
+    fused = None
+    if adapters:
+        fused = S.fuse([S.AdapterPair((torch.randn(K, 16, generator=g) / 64).bfloat16().float(),
+                                      (torch.randn(16, N, generator=g) * 0.02).bfloat16().float(), 16)])
+    s = S.encode(w.cuda(), value_dtype="bf16")
+    ref = _dense_ref(x, w.cuda(), fused).cpu().numpy()
+    n_mc = (M + 127) // 128 if M > 64 else 1
+    seen = set()
+    for ctas in (0, 128 * n_mc, 127, 37):
+        y = S.salr_linear(x, s, fused, num_ctas=ctas)
+        info = _last_launch()
+        seen.add(info["cluster"])
+        assert_close(y.cpu().numpy(), ref, f"M={M} ctas={ctas} {info}")
+        y2 = S.salr_linear(x, s, fused, num_ctas=ctas)
+        assert torch.equal(y, y2)  # run-to-run determinism of every mode
+    assert 0 in seen and max(seen) >= 2, seen

@@ -17,12 +17,13 @@ from paper_2601_16991_b200 import _lib, synthetic
 
 EV = {10: "entry", 0: "setup done", 1: "tma first", 2: "tma last", 3: "prep first", 12: "prep last",
       4: "dec first", 11: "dec last", 5: "mma first", 6: "mma acc_full(last seg)", 7: "epi first acc",
-      8: "epi done", 9: "cta end", 19: "u start (epoch read)", 15: "u claim1 back", 16: "u loads1 done", 17: "u compute1 done", 18: "u slice1 synced", 13: "u slices added", 14: "u ready seen"}
+      8: "epi done", 9: "cta end", 19: "u start (epoch read)", 15: "u claim1 back", 16: "u loads1 done", 17: "u compute1 done", 18: "u slice1 synced", 13: "u slices added", 14: "u ready seen", 20: "ticket (last split seg)", 21: "coop0 wait done", 22: "coop0 reduced", 23: "coop1 wait done", 24: "coop1 reduced", 25: "epi seg0 stored", 26: "final syncthreads", 27: "cluster sync1", 28: "dsmem reduced", 29: "pre-ticket", 30: "ticket back", 31: "last-cta reduced"}
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="gate")
 ap.add_argument("--tokens", type=int, default=1)
 ap.add_argument("--no-adapters", action="store_true")
 ap.add_argument("--launches", type=int, default=4)
+ap.add_argument("--detail", type=int, default=4, help="print the event sequence of the N latest CTAs")
 ap.add_argument("--graph", action="store_true", help="capture the launches (PDL-chained) in one CUDA graph")
 a = ap.parse_args()
 K, N = synthetic.LLAMA3_8B_LINEARS[a.shape]
@@ -76,9 +77,18 @@ for i, b in enumerate(bufs):
         d = (col - t0).double() / 1e3
         print(f"  {name:24s} min {d.min():8.2f}  med {d.median():8.2f}  max {d.max():8.2f} us  (n={col.numel()})")
     prev_end = int(t[:, 9].max())
+    # the latest-finishing CTAs, event by event
+    ends = t[:, 9].clone()
+    for cta in torch.argsort(ends, descending=True)[:a.detail].tolist():
+        evs = sorted((int(t[cta, e]), e) for e in EV if int(t[cta, e]) >= t0)
+        print(f"  cta {cta:3d}: " + "  ".join(f"{EV[e]}@{(v - t0) / 1e3:.2f}" for v, e in evs))
     names = ["tma issue", "prep sees full", "prep done", "dec w4 done", "dec w19 done", "mma issued", "-", "-", "iss start", "iss shfl", "iss empty ok", "iss divmod"]
     print("  CTA0 per-unit (SM clock cycles from CTA entry):")
     print("   unit " + " ".join(f"{names[e]:>14s}" for e in (0, 1, 2, 3, 4, 5, 8, 9, 10, 11)))
+    print("   epilogue seg: before tmem ld / after 1st ld / stored  (cycles)")
+    for sg in range(4):
+        if int(dd[12, sg]):
+            print(f"   seg {sg}: " + " ".join(f"{int(dd[e, sg]) - int(dd[7, 0]):10d}" for e in (12, 13, 14)))
     for i in range(min(24, 64)):
         if int(dd[0, i]) == 0:
             break
