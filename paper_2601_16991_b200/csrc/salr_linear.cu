@@ -123,10 +123,18 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 // per-unit detail for CTA 0 (first 64 units): slot 148*32 + ev*64 + i
+// (compiled in only with -DSALR_UNIT_TRACE: the stamps sit in the per-unit
+// hot loops, where even predicated-off instructions cost issue slots)
+#ifdef SALR_UNIT_TRACE
 #define SALR_TRACE_UNIT(ev, i)                                                               \
   do {                                                                                       \
     if (p.trace && blockIdx.x == 0 && (i) < 64) p.trace[148 * 32 + (ev) * 64 + (i)] = clock64(); \
   } while (0)
+#else
+#define SALR_TRACE_UNIT(ev, i) \
+  do {                         \
+  } while (0)
+#endif
 #define SALR_TRACE(ev) \
   do {                 \
     if (p.trace) p.trace[(size_t)blockIdx.x * 32 + (ev)] = globaltimer(); \
@@ -309,6 +317,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       fence_barrier_init();
     }
     named_bar_sync(2, 64);  // barriers initialised before either producer uses them
+    if (threadIdx.x == 0) SALR_TRACE(21);
     // Start streaming before the CTA-wide setup barrier: this producer's share
     // of the first ring's worth of units of the first output tile (never blocks).
     const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
@@ -316,13 +325,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int pv0 = pv;
     if (producer)
       while (pv < pre) issue_one(false);
+    if (threadIdx.x == 0) SALR_TRACE(23);
     // Weights never depend on the preceding kernel; the input X may (it can
     // be that kernel's output).  Wait for it only now, then send the X tiles
     // of the units already in flight.
     pdl_wait();
+    if (threadIdx.x == 0) SALR_TRACE(24);
     if (lane == 0 && producer)
       for (int v = pv0; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
     __syncwarp();
+    if (threadIdx.x == 0) SALR_TRACE(28);
   }
   // ---- in-kernel U (u_mode 1) geometry.  K is cut into slices of kUSlice
   // rows.  CTA c owns slice c; slices >= G are claimed dynamically.  A_cat is
@@ -361,11 +373,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                          (uint32_t)(min(kUSlice, p.K - pf * kUSlice) * 64 * p.ra * 2));
     }
   }
-  if (warp == kWarpMma) tmem_alloc(tmem_slot, 512);
+  if (warp == kWarpMma) {
+    tmem_alloc(tmem_slot, 512);
+    if (lane == 0) SALR_TRACE(27);
+  }
+  if (threadIdx.x == 32 * kFirstDecWarp) SALR_TRACE(16);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tmem != 0u) __trap();  // all 512 columns are ours: the MMA issuer assumes base 0
   if (threadIdx.x == 0) SALR_TRACE(0);
   const uint32_t a_col0 = (uint32_t)((NACC * ACOLS + 31) & ~31);  // first A-stage column
 
@@ -525,9 +542,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
   } else if (warp == kWarpMma) {
     // ================= MMA issuer: the whole warp walks the schedule (warp-
-    // uniform state stays in uniform registers); one elected lane issues.
+    // uniform state, uniform registers); one elected lane issues.  This
+    // loop is the per-unit serial path of the CTA (it shares its SM
+    // sub-partition with four decoder warps), so per-stage addresses advance
+    // incrementally and each k-tile is one asm block.
+    const uint64_t bdesc0 = desc_kmajor_sw128(smem_u32(xbuf));
+    const uint32_t lo0 = (uint32_t)bdesc0, bhi = (uint32_t)(bdesc0 >> 32);
+    constexpr uint32_t kLoStep = (uint32_t)(BM * 128) >> 4;  // one X stage, 16-byte units
+    // The CTA owns all 512 TMEM columns, so the allocation starts at column
+    // 0 (checked at setup): a compile-time base keeps the MMA operands in
+    // uniform registers.
+    constexpr uint32_t kTm = 0u;
+    const uint32_t atm0 = kTm + a_col0, dec0 = smem_u32(decoded), emp0 = smem_u32(empty);
     int s = 0, seg = 0;
     uint32_t ph = 0, ad_ph = 0;
+    uint32_t lo = lo0, atm = atm0, dad = dec0, ead = emp0;
     bool ready = false;
     int u = u_begin;
     while (u < u_end) {
@@ -535,31 +564,38 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int seg_end = min(u_end, tile_base + p.n_kt);
       const int b = NACC == 2 ? (seg & 1) : 0;
       const uint32_t acc_ph = (uint32_t)((NACC == 2 ? seg >> 1 : seg) & 1);
-      const uint32_t acc = tmem + (uint32_t)(b * ACOLS);
+      const uint32_t acc = kTm + (uint32_t)(b * ACOLS);
       mbar_wait(&acc_empty[b], acc_ph ^ 1);
       tc_fence_after();
       for (int v = u; v < seg_end; ++v) {
-        if (!ready) mbar_wait(&decoded[s], ph);
+        if (!ready) mbar_wait_addr(dad, ph);
         tc_fence_after();
-        // Probe the next unit's barrier now: the ~150-cycle round trip of the
-        // probe overlaps this unit's MMA issue instead of serialising with it.
+        // next stage; probe its barrier now (the probe's round trip overlaps
+        // this unit's issue)
         int s2 = s + 1;
-        uint32_t ph2 = ph;
-        if (s2 == S) { s2 = 0; ph2 ^= 1; }
-        const bool next_ready = (v + 1 < u_end) && mbar_test_wait(&decoded[s2], ph2);
-        if (elect_one()) {
-          const uint64_t bdesc = desc_kmajor_sw128(smem_u32(xbuf + (size_t)s * BM * 128));
-          const uint32_t a_tm = tmem + a_col0 + 32u * s;
-#pragma unroll
-          for (int j = 0; j < kTileK / 16; ++j)
-            mma_ts(acc, a_tm + 8 * j, bdesc + 2 * j, IDESC, (v != u || j) ? 1u : 0u);
-          tc_commit(&empty[s]);
-          if (v == u_begin) SALR_TRACE(5);
-          SALR_TRACE_UNIT(5, v - u_begin);
+        uint32_t ph2 = ph, lo2 = lo + kLoStep, atm2 = atm + 32u, dad2 = dad + 8u, ead2 = ead + 8u;
+        if (s2 == S) {
+          s2 = 0;
+          ph2 ^= 1u;
+          lo2 = lo0;
+          atm2 = atm0;
+          dad2 = dec0;
+          ead2 = emp0;
         }
-        __syncwarp();
+        const bool next_ready = __any_sync(0xffffffffu, (v + 1 < u_end) && mbar_test_addr(dad2, ph2));
+        if (p.dbg & 8) {  // experiment: commit without MMAs (wrong results)
+          if (elect_one()) asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(ead) : "memory");
+          __syncwarp();
+        } else {
+          mma_ktile_ts(acc, atm, lo, bhi, IDESC, v != u ? 1u : 0u, ead);
+        }
+        SALR_TRACE_UNIT(5, v - u_begin);
         s = s2;
         ph = ph2;
+        lo = lo2;
+        atm = atm2;
+        dad = dad2;
+        ead = ead2;
         ready = next_ready;
       }
       if (u == tile_base && p.ra) {

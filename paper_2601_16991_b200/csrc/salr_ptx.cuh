@@ -263,6 +263,62 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// Address-form mbarrier waits (the caller keeps barrier addresses in
+// registers and advances them incrementally).
+__device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t mbar_test_addr(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok;
+}
+// One k-tile of the main MMA chain, issued by one elected lane of a
+// converged warp: 4 x (M=128, K=16) MMAs with A (the decoded W^T tile) in
+// TMEM at a_tm and B (the X tile, K-major SW128) described by {lo, hi},
+// then a commit to the stage's empty barrier.  accumulate == 0 starts the
+// accumulator.  Everything in one asm block: no per-MMA descriptor
+// arithmetic in C, no divergent region around the issue.
+__device__ __forceinline__ void mma_ktile_ts(uint32_t d_tm, uint32_t a_tm, uint32_t lo, uint32_t hi, uint32_t idesc,
+                                             uint32_t accumulate, uint32_t empty_bar) {
+  asm volatile(
+      "{\n\t.reg .pred pe, pa, pt;\n\t"
+      ".reg .b32 l1, l2, l3, a1, a2, a3;\n\t"
+      ".reg .b64 d0, d1, d2, d3;\n\t"
+      "elect.sync _|pe, 0xffffffff;\n\t"
+      "setp.ne.b32 pa, %4, 0;\n\t"
+      "setp.eq.b32 pt, 0, 0;\n\t"
+      "add.u32 l1, %2, 2;\n\t"
+      "add.u32 l2, %2, 4;\n\t"
+      "add.u32 l3, %2, 6;\n\t"
+      "add.u32 a1, %1, 8;\n\t"
+      "add.u32 a2, %1, 16;\n\t"
+      "add.u32 a3, %1, 24;\n\t"
+      "mov.b64 d0, {%2, %3};\n\t"
+      "mov.b64 d1, {l1, %3};\n\t"
+      "mov.b64 d2, {l2, %3};\n\t"
+      "mov.b64 d3, {l3, %3};\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], d0, %5, pa;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], d1, %5, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], d2, %5, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %5, pt;\n\t"
+      "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}" ::"r"(d_tm),
+      "r"(a_tm), "r"(lo), "r"(hi), "r"(accumulate), "r"(idesc), "r"(empty_bar)
+      : "memory");
+}
+
 // Instruction descriptor for kind::f16: bf16 x bf16 -> f32, A and B K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t m, uint32_t n) {
   return (1u << 4)              // D format f32
