@@ -248,6 +248,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   int pv = u_begin + pk;  // next unit to issue (this producer's parity)
   int ps = pk;            // < S whenever this producer is active
   uint32_t pph = 0;
+  const uint64_t pol_stream = l2_policy_evict_first();
   auto load_chunk = [&](int c0, uint32_t& o0, uint32_t& o1) {
     const int v = c0 + (int)lane;
     o0 = o1 = 0u;
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (pv - u_begin >= S) mbar_wait(&empty[ps], pph ^ 1);
     if (lane == 0) {
       const uint32_t bytes = (p.dbg & 2) ? 0u : (o1 - o0) * 16u;
-      if (bytes) bulk_g2s(recbuf + (size_t)ps * p.rec_slot, p.records + (size_t)o0 * 16u, bytes, &full[ps]);
+      if (bytes) bulk_g2s_hint(recbuf + (size_t)ps * p.rec_slot, p.records + (size_t)o0 * 16u, bytes, &full[ps], pol_stream);
       if (with_x) issue_x(pv, ps);
       mbar_arrive_expect_tx(&full[ps], bytes + BM * 128);
       SALR_TRACE_UNIT(0, pv - u_begin);

@@ -147,6 +147,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Same, with an L2 cache-policy hint (createpolicy): the weight records are
+// read exactly once per launch, so they stream through L2 as evict-first and
+// leave the small, reused data (tile offsets, X, U, adapters) resident.
+__device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 // 2-D tiled tensor copy global -> shared (box defined by the tensor map).
 __device__ __forceinline__ void tma_2d_g2s(void* dst_smem, const CUtensorMap* map, int32_t c0,
                                            int32_t c1, uint64_t* bar) {
