@@ -1,0 +1,121 @@
+"""Turn the raw outputs of tools/gpu_bench_profile.sh (gpurun_out/) into the
+tracked evidence under profiles/ (round tag, e.g. r01).
+
+    python tools/summarize_profiles.py r01
+
+Reads gpurun_out/{bench.json, bench_ref.json, bl_all.jsonl, bl_prefill.jsonl,
+sweep.jsonl, launches.csv, prof_gate32.ncu-rep, prof_gate1.ncu-rep} and writes
+profiles/<tag>_*.{json,jsonl,csv} plus profiles/ncu_summary.json (bench.py
+reads `traffic_bytes_per_launch` from it).  Needs `ncu` on PATH for the
+.ncu-rep files (it is in this image).
+"""
+import csv
+import io
+import json
+import os
+import shutil
+import subprocess
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(REPO, "gpurun_out")
+PROF = os.path.join(REPO, "profiles")
+TILES_GATE = 112 * 64  # 64x128 tiles of the 4096x14336 gate linear
+
+
+def last_json_line(path):
+    with open(path) as f:
+        lines = [l for l in f if l.startswith("{")]
+    return json.loads(lines[-1])
+
+
+def ncu_raw(rep):
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                         check=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    return [dict(zip(rows[0], r)) for r in rows[2:]], dict(zip(rows[0], rows[1]))
+
+
+def f(v):
+    return float(str(v).replace(",", ""))
+
+
+def main(tag):
+    os.makedirs(PROF, exist_ok=True)
+    b = last_json_line(os.path.join(OUT, "bench.json"))
+    json.dump(b, open(os.path.join(PROF, f"{tag}_bench_stack.json"), "w"), indent=1)
+    r = last_json_line(os.path.join(OUT, "bench_ref.json"))
+    json.dump(r, open(os.path.join(PROF, f"{tag}_bench_reference_arm.json"), "w"), indent=1)
+    for src, dst in (("bl_all.jsonl", "per_linear_decode.jsonl"), ("bl_prefill.jsonl", "per_linear_prefill.jsonl"),
+                     ("sweep.jsonl", "sweep_4096x14336.jsonl")):
+        p = os.path.join(OUT, src)
+        if os.path.exists(p):
+            shutil.copy(p, os.path.join(PROF, f"{tag}_{dst}"))
+
+    # launch list: per-launch duration and DRAM bytes of our kernels
+    rows = list(csv.reader(open(os.path.join(OUT, "launches.csv"))))
+    hdr = next(i for i, row in enumerate(rows) if "Metric Name" in row)
+    h = rows[hdr]
+    idx = {k: h.index(k) for k in ("ID", "Kernel Name", "Metric Name", "Metric Value")}
+    launches = {}
+    for row in rows[hdr + 1:]:
+        if len(row) < len(h):
+            continue
+        lid = int(row[idx["ID"]])
+        d = launches.setdefault(lid, {"id": lid, "kernel": row[idx["Kernel Name"]]})
+        name, val = row[idx["Metric Name"]], f(row[idx["Metric Value"]])
+        if name == "gpu__time_duration.sum":
+            d["us"] = val / 1e3 if val > 1e4 else val  # ns or us depending on ncu units
+        elif name.startswith("dram__bytes"):
+            d["dram_bytes"] = d.get("dram_bytes", 0.0) + val
+    ll = sorted(launches.values(), key=lambda d: d["id"])
+    share = {}
+    tot = sum(d.get("us", 0.0) for d in ll)
+    for d in ll:
+        s = share.setdefault(d["kernel"], {"launches": 0, "total_us": 0.0})
+        s["launches"] += 1
+        s["total_us"] += d.get("us", 0.0)
+    for s in share.values():
+        s["share"] = s["total_us"] / tot if tot else None
+    json.dump({"note": "ncu --metrics gpu__time_duration.sum,dram__bytes_* --clock-control none over "
+                       "`bench.py --layers 1` (kernel filter salr_*|adapter_u); per-launch times are cold-cache "
+                       "and serialised: compare shares, not absolutes",
+               "share_by_kernel": share, "launches": ll},
+              open(os.path.join(PROF, f"{tag}_launch_list.json"), "w"), indent=1)
+
+    summ = {}
+    for name, tokens in (("prof_gate32", 32), ("prof_gate1", 1)):
+        rep = os.path.join(OUT, name + ".ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        recs, units = ncu_raw(rep)
+        m = recs[0]
+        dur = f(m["gpu__time_duration.sum"])
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd = f(m["dram__bytes_read.sum"]) * scale[units["dram__bytes_read.sum"]]
+        wr = f(m["dram__bytes_write.sum"]) * scale[units["dram__bytes_write.sum"]]
+        summ[name] = {
+            "kernel": "salr_linear_kernel (gate 4096x14336, p=0.5, r16+r16 adapters, TB2 compute format)",
+            "tokens": tokens,
+            "duration_us_under_ncu": dur,
+            "dram_read_bytes": rd,
+            "dram_write_bytes": wr,
+            "traffic_bytes_per_launch": rd + wr,
+            "algorithmic_compressed_bytes": 65950928,
+            "smem_lsu_wavefronts_per_tile": f(m["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]) / TILES_GATE,
+            "warp_instructions_per_tile": f(m["smsp__inst_executed.sum"]) / TILES_GATE,
+            "ipc_active": f(m["sm__inst_executed.avg.per_cycle_active"]),
+            "tensor_pipe_pct_elapsed": f(m["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]),
+            "note": "ncu --set full --clock-control none, cold cache, serialized",
+        }
+        with open(os.path.join(PROF, f"{tag}_ncu_{name}_details.csv"), "w") as fo:
+            fo.write(subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
+                                    text=True).stdout)
+    if "prof_gate32" in summ:
+        summ["traffic_bytes_per_launch"] = summ["prof_gate32"]["traffic_bytes_per_launch"]
+    json.dump(summ, open(os.path.join(PROF, "ncu_summary.json"), "w"), indent=1)
+    print(json.dumps({k: v for k, v in summ.items() if k != "traffic_bytes_per_launch"}, indent=1))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
