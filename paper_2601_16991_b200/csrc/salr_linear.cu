@@ -97,6 +97,7 @@ constexpr int kFirstDecWarp = 4;
 constexpr int kFirstEpiWarp = 20;
 constexpr uint32_t kAdTileBytes = 128 * 128;   // B_cat^T tile: 128 rows x 64 bf16
 constexpr size_t kSmemMax = 232448;            // 227 KB opt-in per block
+constexpr int64_t kPrefillMinM = 256;          // M above this: salr_prefill_kernel
 
 __host__ __device__ constexpr int nacc_for(int bm) { return bm <= 128 ? 2 : 1; }
 __host__ __device__ constexpr int acc_cols_for(int bm) { return bm < 32 ? 32 : bm; }
@@ -1205,6 +1206,8 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t co
   return SALR_OK;
 }
 
+#include "salr_prefill.cuh"
+
 static unsigned long long* g_trace = nullptr;  // set by salr_debug_set_trace (tools only)
 
 static int pick_bm(int64_t M) {
@@ -1319,6 +1322,39 @@ static int launch_linear(const CUtensorMap* maps, const LinearParams& p, int cta
     case 2: return launch_linear_g<BM, 2>(maps, p, ctas, s, pdl);
     default: return launch_linear_g<BM, 4>(maps, p, ctas, s, pdl);
   }
+}
+
+// Prefill kernel: deepest X ring (and a 4-slot record ring) that fits.
+static int launch_prefill(const CUtensorMap* maps, PrefillParams pp, cudaStream_t s, bool pdl) {
+  pp.SR = 6;
+  pp.SX = 12;
+  while (pp.SX > 2 && pf_plan(pp.SR, pp.SX, pp.ra, pp.rec_slot).total > kSmemMax) --pp.SX;
+  const PfPlan plan = pf_plan(pp.SR, pp.SX, pp.ra, pp.rec_slot);
+  SALR_CHECK_ARG(plan.total <= kSmemMax, SALR_ERR_CONFIG, "prefill smem plan does not fit");
+  pp.w_off = plan.w_off;
+  pp.x_off = plan.x_off;
+  pp.b_off = plan.b_off;
+  pp.rec_off = plan.rec_off;
+  pp.bar_off = plan.bar_off;
+  static bool attr_done = false;
+  if (!attr_done) {
+    SALR_CUDA_TRY(cudaFuncSetAttribute(salr_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)std::min<int64_t>(sm_count(), pp.items));
+  cfg.blockDim = dim3(kPfThreads);
+  cfg.dynamicSmemBytes = plan.total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  SALR_CUDA_TRY(cudaLaunchKernelEx(&cfg, salr_prefill_kernel, maps[0], maps[1], maps[2], maps[3], pp));
+  const int info[12] = {(int)cfg.gridDim.x, pp.SX, 128, -1, pp.ra ? 2 : 0, 0, 0, pdl ? 1 : 0, 0, -1, (int)plan.total, 1};
+  for (int i = 0; i < 12; ++i) g_last_launch[i] = info[i];
+  return SALR_OK;
 }
 
 static inline size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
@@ -1510,6 +1546,30 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
         u_lo);
     SALR_LAUNCH_CHECK();
     pdl = true;
+  }
+  static const bool no_prefill = getenv("SALR_NO_PREFILL") != nullptr;
+  const int64_t pf_items = ((M + 128 * kPfMG - 1) / (128 * kPfMG)) * p.n_nt;
+  // The prefill kernel has no split-K: it needs enough (512-token x
+  // 128-column) items to occupy the GPU (measured crossover ~3/4 of the SMs).
+  if (M > kPrefillMinM && num_ctas <= 0 && !no_prefill && 4 * pf_items >= 3 * (int64_t)sm_count()) {
+    // prefill-size M: decode each weight tile once per 512 tokens
+    PrefillParams pp = {};
+    pp.records = records;
+    pp.tile_off = tile_off;
+    pp.y = y;
+    pp.y_dtype = y_dtype;
+    pp.ldy = (int)ldy;
+    pp.M = (int)M;
+    pp.N = (int)N;
+    pp.n_kt = p.n_kt;
+    pp.n_nt = p.n_nt;
+    pp.n_mg = (int)((M + 128 * kPfMG - 1) / (128 * kPfMG));
+    pp.items = pp.n_mg * pp.n_nt;
+    pp.ra = ra;
+    pp.rec_slot = p.rec_slot;
+    pp.trace = g_trace;
+    pp.dbg = p.dbg;
+    return launch_prefill(maps, pp, s, pdl);
   }
   switch (bm) {
     case 16: rc = launch_linear<16>(maps, p, (int)ctas, s, pdl); break;
