@@ -193,3 +193,34 @@ def test_split_k_reduction_modes(S, M, adapters):
         y2 = S.salr_linear(x, s, fused, num_ctas=ctas)
         assert torch.equal(y, y2)  # run-to-run determinism of every mode
     assert 0 in seen and max(seen) >= 2, seen
+
+
+@pytest.mark.parametrize("rank", [16, 64])
+@pytest.mark.parametrize("out_dtype", ["f32", "bf16"])
+def test_prefill_kernel_ragged(S, rank, out_dtype):
+    """The prefill kernel (M > 256 with >= 3/4 of the SMs worth of 512-token x
+    128-column items): ragged M (partial 128-token chunk), K (partial k-tile)
+    and N (partial last column tile), adapters with one and two 64-rank
+    blocks, fp32 and bf16 output."""
+    g = torch.Generator().manual_seed(4242 + rank)
+    M, K, N = 300, 200, 14300
+    w = (torch.randn(K, N, generator=g) * 0.05).bfloat16().float()
+    w[torch.rand(K, N, generator=g) < 0.5] = 0
+    x = torch.randn(M, K, generator=g).bfloat16().float().cuda()
+    fused = S.fuse([S.AdapterPair((torch.randn(K, rank, generator=g) / 16).bfloat16().float(),
+                                  (torch.randn(rank, N, generator=g) * 0.05).bfloat16().float(), rank),
+                    S.AdapterPair((torch.randn(K, rank, generator=g) / 16).bfloat16().float(),
+                                  (torch.randn(rank, N, generator=g) * 0.05).bfloat16().float(), rank, 2.0)])
+    s = S.encode(w.cuda(), value_dtype="bf16")
+    ref = _dense_ref(x, w.cuda(), fused).cpu().numpy()
+    dt = torch.float32 if out_dtype == "f32" else torch.bfloat16
+    y = S.salr_linear(x, s, fused, out_dtype=dt)
+    info = _last_launch()
+    assert info["smem"] > 0 and info["groups"] == -1, info  # the prefill kernel ran
+    if out_dtype == "f32":
+        assert_close(y.cpu().numpy(), ref, f"prefill r={rank}")
+    else:
+        yb = y.double().cpu().numpy()
+        err = np.abs(yb - ref)
+        assert (err <= 2.0 ** -8 * np.abs(ref) + 2e-3 * np.abs(ref).max()).all(), err.max()
+    assert torch.equal(y, S.salr_linear(x, s, fused, out_dtype=dt))
