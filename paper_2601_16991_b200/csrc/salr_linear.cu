@@ -114,7 +114,7 @@ __host__ __device__ inline SmemPlan smem_plan(int bm, int stages, int ra, uint32
   p.rec_off = p.x_off + (uint32_t)stages * bm * 128u;      // stages x kRecSlot
   p.base_off = p.rec_off + (uint32_t)stages * rec_slot;    // stages x 256 u32
   p.bar_off = p.base_off;
-  p.total = p.bar_off + 8u * (3u * stages + 6u) + 16u + 1024u;  // + tmem slot + alignment slack
+  p.total = p.bar_off + 8u * (4u * stages + 6u) + 16u + 1024u;  // + tmem slot + alignment slack
   return p;
 }
 
@@ -206,7 +206,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
   uint64_t* empty = full + S;
   uint64_t* decoded = empty + S;
-  uint64_t* acc_full = decoded + S;    // [2]
+  // X tiles complete on their own barriers: the decoders wait only for the
+  // records, which are in flight before the programmatic-launch wait, so
+  // they decode the first ring while the preceding kernel drains; the MMA
+  // waits for both
+  uint64_t* xfull = decoded + S;
+  uint64_t* acc_full = xfull + S;      // [2]
   uint64_t* acc_empty = acc_full + 2;  // [2]
   uint64_t* ad_full = acc_empty + 2;
   uint64_t* ad_empty = ad_full + 1;
@@ -264,7 +269,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   auto issue_x = [&](int v, int st) {
     const int kt = v % p.n_kt;
     const int mc = v / tiles_per_mc;
-    tma_2d_g2s(xbuf + (size_t)st * BM * 128, &xmap, kt * kTileK, mc * BM, &full[st]);
+    tma_2d_g2s(xbuf + (size_t)st * BM * 128, &xmap, kt * kTileK, mc * BM, &xfull[st]);
+    mbar_arrive_expect_tx(&xfull[st], BM * 128);
   };
   // Issue unit pv.  The copies go out before arrive.expect_tx (the phase
   // cannot complete before the arrive, and issuing the copy first keeps it
@@ -283,8 +289,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (lane == 0) {
       const uint32_t bytes = (p.dbg & 2) ? 0u : (o1 - o0) * 16u;
       if (bytes) bulk_g2s_hint(recbuf + (size_t)ps * p.rec_slot, p.records + (size_t)o0 * 16u, bytes, &full[ps], pol_stream);
+      mbar_arrive_expect_tx(&full[ps], bytes);
       if (with_x) issue_x(pv, ps);
-      mbar_arrive_expect_tx(&full[ps], bytes + BM * 128);
       SALR_TRACE_UNIT(0, pv - u_begin);
     }
     __syncwarp();
@@ -306,6 +312,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       }
       for (int s = 0; s < S; ++s) {
         mbar_init(&full[s], 1);
+        mbar_init(&xfull[s], 1);
         mbar_init(&empty[s], 1);
         mbar_init(&decoded[s], WPG);
       }
@@ -324,19 +331,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // of the first ring's worth of units of the first output tile (never blocks).
     const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
     const int pre = min(first_seg_end, u_begin + S);
-    const int pv0 = pv;
     if (producer)
       while (pv < pre) issue_one(false);
     if (threadIdx.x == 0) SALR_TRACE(23);
-    // Weights never depend on the preceding kernel; the input X may (it can
-    // be that kernel's output).  Wait for it only now, then send the X tiles
-    // of the units already in flight.
-    pdl_wait();
-    if (threadIdx.x == 0) SALR_TRACE(24);
-    if (lane == 0 && producer)
-      for (int v = pv0; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
-    __syncwarp();
-    if (threadIdx.x == 0) SALR_TRACE(28);
   }
   // ---- in-kernel U (u_mode 1) geometry.  K is cut into slices of kUSlice
   // rows.  CTA c owns slice c; slices >= G are claimed dynamically.  A_cat is
@@ -521,7 +518,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   }
 
   if (warp == kWarpProd0 || warp == kWarpProd1) {
-    // ================= TMA producers
+    // ================= TMA producers.  Weights never depend on the preceding
+    // kernel; the input X may (it can be that kernel's output): wait for it
+    // only now -- after the CTA-wide setup, so the decoders already work on
+    // the first ring -- then send the X tiles of the units already in flight.
+    pdl_wait();
+    if (threadIdx.x == 0) SALR_TRACE(24);
+    if (lane == 0 && producer) {
+      const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
+      const int pre = min(first_seg_end, u_begin + S);
+      for (int v = u_begin + pk; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) SALR_TRACE(28);
     if (lane == 0 && pk == 0) SALR_TRACE(1);
     if (producer)
       while (pv < u_end) issue_one(true);
@@ -571,6 +580,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       tc_fence_after();
       for (int v = u; v < seg_end; ++v) {
         if (!ready) mbar_wait_addr(dad, ph);
+        mbar_wait_addr(dad + 8u * (uint32_t)S, ph);  // this stage's X tile (xfull)
         tc_fence_after();
         // next stage; probe its barrier now (the probe's round trip overlaps
         // this unit's issue)

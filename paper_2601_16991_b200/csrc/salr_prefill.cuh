@@ -138,7 +138,6 @@ __global__ void __launch_bounds__(kPfThreads, 1)
     for (int it = blockIdx.x; it < p.items; it += G) {
       int mg, nt, mgc;
       item_geom(it, mg, nt, mgc);
-      const int row0 = mg * kPfMG * 128;
       if (p.ra) {
         if (lane == 0) {
           mbar_wait(b_empty, bph ^ 1);
