@@ -758,6 +758,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       // swizzle) built from the fixed-point U or loaded by TMA.
       if (etid == 0) {
         while (!mbar_test_wait(ad_empty, ad_ph ^ 1)) __nanosleep(64);
+        // the B_cat^T tile does not depend on U: start its fetch now (the
+        // transaction bytes are expected below, with the single arrive)
+        for (int a = 0; a < p.ra; ++a)
+          tma_2d_g2s(adbuf + (size_t)a * (kAdTileBytes + 2u * BM * 128u), &bmap, 64 * a, nt * kTileN, ad_full);
       }
       named_bar_sync(1, 128);
       if (p.u_mode == 1) {
@@ -803,7 +807,6 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         mbar_arrive_expect_tx(ad_full, (uint32_t)p.ra * (kAdTileBytes + ubytes));
         for (int a = 0; a < p.ra; ++a) {
           uint8_t* blk = adbuf + (size_t)a * (kAdTileBytes + 2u * BM * 128u);
-          tma_2d_g2s(blk, &bmap, 64 * a, nt * kTileN, ad_full);
           if (p.u_mode == 2) {
             tma_2d_g2s(blk + kAdTileBytes, &uhimap, 64 * a, mc * BM, ad_full);
             tma_2d_g2s(blk + kAdTileBytes + BM * 128, &ulomap, 64 * a, mc * BM, ad_full);
