@@ -224,3 +224,47 @@ def test_prefill_kernel_ragged(S, rank, out_dtype):
         err = np.abs(yb - ref)
         assert (err <= 2.0 ** -8 * np.abs(ref) + 2e-3 * np.abs(ref).max()).all(), err.max()
     assert torch.equal(y, S.salr_linear(x, s, fused, out_dtype=dt))
+
+
+@pytest.mark.parametrize("M", [1, 8, 32])
+def test_pdl_chain_matches_serial(S, M):
+    """Programmatic-dependent chains (as in the stack): every linear reads the
+    previous one's output and the launches overlap; the in-kernel U epochs,
+    split-K tickets and alternating workspaces must give exactly the serial
+    results, eagerly and replayed from a CUDA graph."""
+    g = torch.Generator().manual_seed(900 + M)
+    K = 1024
+    mats, fus = [], []
+    for i in range(4):
+        w = (torch.randn(K, K, generator=g) * 0.03).bfloat16().float()
+        w[torch.rand(K, K, generator=g) < 0.5] = 0
+        s = S.encode(w.cuda(), value_dtype="bf16")
+        s.compute_format()
+        mats.append(s)
+        fus.append(S.fuse([S.AdapterPair((torch.randn(K, 16, generator=g) / 32).bfloat16().float(),
+                                         (torch.randn(16, K, generator=g) * 0.03).bfloat16().float(), 16)]))
+        fus[-1].device_operands()
+    x = torch.randn(M, K, generator=g).bfloat16().cuda()
+
+    def chain(pdl, outs):
+        h = x
+        for i in range(12):
+            h = S.salr_linear(h, mats[i % 4], fus[i % 4], out=outs[i], out_dtype=torch.bfloat16,
+                              check_finite=False, pdl=pdl)
+        return outs
+
+    ref = chain(False, [torch.empty(M, K, device="cuda", dtype=torch.bfloat16) for _ in range(12)])
+    got = chain(True, [torch.empty(M, K, device="cuda", dtype=torch.bfloat16) for _ in range(12)])
+    torch.cuda.synchronize()
+    for i in range(12):
+        assert torch.equal(ref[i], got[i]), i
+    outs = [torch.empty(M, K, device="cuda", dtype=torch.bfloat16) for _ in range(12)]
+    chain(True, outs)  # warm-up outside capture (workspaces, formats)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        chain(True, outs)
+    for _ in range(3):
+        graph.replay()
+        torch.cuda.synchronize()
+        for i in range(12):
+            assert torch.equal(ref[i], outs[i]), i
