@@ -4,40 +4,40 @@
 // bitmap decode into tiles, stage-2 tile products, adapter delta added once),
 // pkg/src/salr/fusion.py:87-92 (apply_fused: exactly two products).
 //
-// B200 design (DESIGN.md section 3):
+// B200 design (DESIGN.md section 4):
 //   * swap-AB: the tensor core computes a Y^T tile = W^T tile (128 output
 //     columns = M_mma 128) x X^T (N_mma = BM tokens), fp32 accumulator in TMEM.
-//   * warp roles of one persistent CTA per SM (24 warps):
-//       warp 0      TMA producer: each compressed tile record (1-D bulk copy)
-//                   and its X tile (2-D tensor map, 128B swizzle) into a ring
-//                   of shared-memory stages (full/empty mbarriers, expect_tx);
-//                   adapter operands (B_cat^T tile, U hi/lo) per output tile.
-//       warp 1      MMA issuer (one thread), TMEM allocator.
-//       warp 2      row-base warp: per stage, the exclusive prefix of the
-//                   bitmap row popcounts (warp scan) -> smem table of the
-//                   shared-memory byte offset where every (group, row) run of
-//                   compacted values starts.
-//       warps 4-19  decoders, four groups of four warps.  Group t decodes
-//                   tiles it = t (mod 4); warp (t, q) owns output columns
-//                   32q..32q+31 == TMEM lanes 32q..32q+31 and expands all 64
-//                   rows of that column group: value = bits & lanebit ?
-//                   vals[rowbase + popc(bits & lanemask_lt)] : 0, packed as
-//                   bf16 pairs along K and written with tcgen05.st straight
+//   * warp roles of one persistent CTA per SM (25 warps):
+//       warps 0, 24 TMA producers (even / odd work units): each TB2 record
+//                   (1-D bulk copy, L2 evict-first) into a ring of up to 8
+//                   shared-memory stages (full/empty mbarriers, expect_tx),
+//                   the X tile (2-D tensor map, 128B swizzle) on its own
+//                   barrier; records of the first ring go out before the
+//                   programmatic-launch wait.
+//       warp 1      MMA issuer (one elected lane), TMEM allocator.
+//       warp 2      publisher: releases the CTA's first split-K partial.
+//       warps 4-19  decoders, four groups of four warps.  Group g decodes
+//                   units = g (mod 4); warp (g, q) owns output columns
+//                   32q..32q+31 == TMEM lanes 32q..32q+31, expands the 64
+//                   rows of its column from the band runs of the TB2 record
+//                   and writes bf16 pairs along K with tcgen05.st straight
 //                   into the TMEM A operand of the next MMA -- decoded tiles
 //                   never touch shared memory.
-//       warps 20-23 epilogue: TMEM accumulator -> registers -> Y (or an fp32
-//                   split-K partial + fixed-order fixup).
+//       warps 20-23 epilogue: in-kernel U = X @ A_cat (warp-level mma.sync,
+//                   int64 fixed-point atomics), adapter operands, TMEM
+//                   accumulator -> Y or an fp32 split-K partial.
 //   * the ring is the GPU form of the reference's SPSC _Ring
 //     (pipeline.py:110-183): decode of tile k+1 overlaps the MMA of tile k.
-//   * adapters: U = X @ A_cat is produced by a small pre-kernel (PDL
-//     overlapped) as bf16 hi + lo halves; the CTA that owns k-tile 0 of an
-//     output tile adds B_cat^T x [U_hi | U_lo]^T into the SAME TMEM
-//     accumulator (two SMEM-operand MMAs), so Y leaves the chip once.
+//   * adapters: the CTA that owns k-tile 0 of an output tile adds
+//     B_cat^T x [U_hi | U_lo]^T into the SAME TMEM accumulator (two
+//     SMEM-operand MMAs), so Y leaves the chip once.
 //   * stream-K: every CTA owns a contiguous range of (m-chunk, n-tile, k-tile)
-//     work units; a CTA that covers only part of an output tile's K range
-//     stores its fp32 partial tile and the last CTA to finish that tile sums
-//     the partials in a fixed CTA order -- results are bit-identical from run
-//     to run (the reference's schedule independence, test_pipeline.py:90-112).
+//     work units; split output tiles are summed in a fixed CTA order through
+//     DSMEM (thread-block clusters) or global memory -- results are
+//     bit-identical from run to run (the reference's schedule independence,
+//     test_pipeline.py:90-112).
+//   * M > 256: salr_prefill.cuh (one decode per weight tile per 512 tokens).
+
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
