@@ -551,6 +551,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       __syncwarp();
       named_bar_arrive(6, 160);
     }
+    if (p.u_mode == 1) {
+      // epoch ticket: the last CTA to finish with U advances the epoch (flips
+      // the U parity) for the next launch on this workspace
+      named_bar_sync(7, 160);
+      if (lane == 0) {
+        fence_acq_rel_gpu();
+        const uint32_t d = atomicAdd(p.ctrl + kCtrlDone, 1u);
+        if (d + 1 == (uint32_t)G) {
+          p.ctrl[kCtrlDone] = 0u;
+          fence_acq_rel_gpu();
+          p.ctrl[kCtrlEpoch] = p.ctrl[kCtrlEpoch] + 1u;
+        }
+      }
+      __syncwarp();
+    }
   } else if (warp == kWarpMma) {
     // ================= MMA issuer: the whole warp walks the schedule (warp-
     // uniform state, uniform registers); one elected lane issues.  This
@@ -998,28 +1013,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int jpub = early_pub ? 1 : 0;
     if (nsplit > jpub) named_bar_sync(1, 128);  // every partial of this CTA stored (CTA scope)
     if (early_pub) named_bar_sync(6, 160);  // the publisher's ticket value is in
-    if (etid == 0 && (nsplit || p.u_mode == 1)) {
+    // this CTA is done with U: the publisher warp takes the epoch ticket
+    // off the epilogue's critical path
+    if (p.u_mode == 1) named_bar_arrive(7, 160);
+    if (etid == 0 && nsplit) {
       SALR_TRACE(29);
       uint32_t old[2] = {early_pub ? *early_old_slot : 0u, 0u};
-      // acq_rel: publishes the last partial and acquires the others' (and
-      // orders this CTA's U reads before the epoch ticket below)
+      // acq_rel: publishes the last partial and acquires the others'
       if (nsplit > jpub) old[nsplit - 1] = ticket_add_acq_rel(tile_ticket(tl[nsplit - 1]), 1u);
-      else if (p.u_mode == 1) fence_acq_rel_gpu();
       uint32_t lf = 0;
 #pragma unroll
       for (int j = 0; j < nsplit; ++j)
         if (!p.coop && old[j] + 1 == (uint32_t)tile_np(tl[j])) lf |= 1u << j;
-      if (p.u_mode == 1) {
-        // this CTA's U slices are published and its U reads done; the last
-        // CTA advances the epoch (flips the U parity) for the next launch on
-        // this workspace
-        const uint32_t d = atomicAdd(p.ctrl + kCtrlDone, 1u);
-        if (d + 1 == (uint32_t)G) {
-          p.ctrl[kCtrlDone] = 0u;
-          fence_acq_rel_gpu();
-          p.ctrl[kCtrlEpoch] = p.ctrl[kCtrlEpoch] + 1u;
-        }
-      }
       *last_flag = lf;
       SALR_TRACE(30);
     }
