@@ -551,6 +551,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       __syncwarp();
       named_bar_arrive(6, 160);
     }
+    if (p.coop && !p.cluster && u_begin < u_end) {
+      // the CTA's last split partial (coop path): same release + ticket
+      const int t0 = u_begin - u_begin % p.n_kt, t1 = (u_end - 1) - (u_end - 1) % p.n_kt;
+      int nsp = 0, tlast = 0;
+      if (!(t0 >= u_begin && t0 + p.n_kt <= u_end)) { ++nsp; tlast = t0; }
+      if (t1 != t0 && !(t1 >= u_begin && t1 + p.n_kt <= u_end)) { ++nsp; tlast = t1; }
+      if (nsp > (early_split ? 1 : 0)) {
+        named_bar_sync(8, 160);  // epilogue: partial stored (bar.arrive)
+        if (lane == 0) {
+          fence_acq_rel_gpu();  // release (barrier + cumulativity)
+          atomicAdd(&p.tickets[(tlast / tiles_per_mc) * p.n_nt + (tlast / p.n_kt) % p.n_nt], 1u);
+        }
+        __syncwarp();
+      }
+    }
     if (p.u_mode == 1) {
       // epoch ticket: the last CTA to finish with U advances the epoch (flips
       // the U parity) for the next launch on this workspace
@@ -1015,8 +1030,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (early_pub) named_bar_sync(6, 160);  // the publisher's ticket value is in
     // this CTA is done with U: the publisher warp takes the epoch ticket
     // off the epilogue's critical path
+    // coop: the publisher warp releases the last partial too (nobody here
+    // needs the ticket's old value)
+    if (p.coop && nsplit > jpub) named_bar_arrive(8, 160);
     if (p.u_mode == 1) named_bar_arrive(7, 160);
-    if (etid == 0 && nsplit) {
+    if (etid == 0 && nsplit && !p.coop) {
       SALR_TRACE(29);
       uint32_t old[2] = {early_pub ? *early_old_slot : 0u, 0u};
       // acq_rel: publishes the last partial and acquires the others'
