@@ -342,7 +342,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // dynamically claimed ones are prefetched into L2.  (Everything U-related
   // is recomputed where used: nothing stays live across the decode loops.)
   constexpr int kSX = kUSlice + 8;  // X chunk row stride (pads: conflict-free
-  auto u_geom_wide = [&]() { return (p.dbg & 4) ? false : ((u_end - u_begin) < 24 && p.M >= 16); };
+  auto u_geom_wide = [&]() { return (p.dbg & 4) ? false : ((u_end - u_begin) < 8 && p.M >= 16); };
   auto u_kSA = [&]() { return 64 * p.ra + 8; };  // A slice row stride   mma fragment loads)
   auto u_staged_fn = [&]() {
     return (p.K % 8 == 0) &&
@@ -388,9 +388,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // ---- in-kernel U = X @ A_cat (u_mode 1): each slice partial goes into
   // the int64 fixed-point accumulator (integer atomics: order-independent,
   // bit-reproducible) and is published at once (slices-done counter).
-  // Participants: the epilogue warps, plus the decoder warps for short
-  // launches with M >= 16 (work-bound partials); with few tokens it is
-  // latency-bound.
+  // Participants: the epilogue warps, plus the decoder warps when a CTA has
+  // fewer than 8 units and M >= 16 (work-bound partials, little decode to
+  // delay; measured: with 16 units per CTA the decoders are better off
+  // starting to decode).
   const bool u_wide = u_geom_wide();
   const int kUThreads = u_wide ? 640 : 128;
   if (p.u_mode == 1 && warp >= (u_wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4) {
