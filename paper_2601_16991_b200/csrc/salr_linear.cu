@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       // B_cat^T tile by TMA, U hi/lo (BM x 64 per rank block, K-major, 128B
       // swizzle) built from the fixed-point U or loaded by TMA.
       if (etid == 0) {
-        while (!mbar_test_wait(ad_empty, ad_ph ^ 1)) __nanosleep(64);
+        mbar_wait(ad_empty, ad_ph ^ 1);
         // the B_cat^T tile does not depend on U: start its fetch now (the
         // transaction bytes are expected below, with the single arrive)
         for (int a = 0; a < p.ra; ++a)
@@ -940,8 +940,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int mc = u / (p.n_kt * p.n_nt);
       const int b = NACC == 2 ? (seg & 1) : 0;
       const uint32_t acc_ph = (uint32_t)((NACC == 2 ? seg >> 1 : seg) & 1);
-      // long wait: poll gently so the spinning warps do not steal issue slots
-      while (!mbar_test_wait(&acc_full[b], acc_ph)) __nanosleep(256);
+      // long wait: try_wait suspends the warp in hardware (no issue slots)
+      // and wakes it as soon as the phase completes
+      mbar_wait(&acc_full[b], acc_ph);
       tc_fence_after();
       if (etid == 0 && seg == 0) SALR_TRACE(7);
       // partial slot of this CTA: 0 for its first segment, 1 otherwise
