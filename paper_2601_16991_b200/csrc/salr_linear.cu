@@ -97,6 +97,7 @@ constexpr int kFirstDecWarp = 4;
 constexpr int kFirstEpiWarp = 20;
 constexpr uint32_t kAdTileBytes = 128 * 128;   // B_cat^T tile: 128 rows x 64 bf16
 constexpr size_t kSmemMax = 232448;            // 227 KB opt-in per block
+constexpr size_t kSmemMaxLinear = kSmemMax - 128;  // minus the decoders' static nibble table
 constexpr int64_t kPrefillMinM = 256;          // M above this: salr_prefill_kernel
 
 __host__ __device__ constexpr int nacc_for(int bm) { return bm <= 128 ? 2 : 1; }
@@ -105,6 +106,23 @@ __host__ __device__ constexpr int acc_cols_for(int bm) { return bm < 32 ? 32 : b
 struct SmemPlan {
   uint32_t x_off, rec_off, base_off, ad_off, bar_off, total;
 };
+
+// Nibble expansion table of the decoder.  For the 4-bit column mask n of a
+// 4-row band (bit i = row i present) whose values start at halfword s:
+//   word 0 (rows 0,1) = prmt(v[s],   v[s+1],   sel(n & 3))
+//   word 1 (rows 2,3) = prmt(v[s+c], v[s+c+1], sel(n >> 2)),  c = popc(n & 3)
+// with each v[] loaded zero-extended to 32 bits, so bytes 2,3 of the first
+// source are zero: sel(00) = 0x3232 (0), sel(01) = 0x3210 ([v, 0]),
+// sel(10) = 0x1032 ([0, v]), sel(11) = 0x5410 ([v, v']).  Entry =
+// sel(n & 3) | (2c) << 16 (low word; prmt reads only bits 0-15) and
+// sel(n >> 2) (high word).
+__host__ __device__ constexpr uint32_t nib_sel(uint32_t x) {
+  return x == 0 ? 0x3232u : x == 1 ? 0x3210u : x == 2 ? 0x1032u : 0x5410u;
+}
+__host__ __device__ constexpr uint64_t nib_lut_entry(uint32_t n) {
+  return (uint64_t)(nib_sel(n & 3u) | ((2u * ((n & 1u) + ((n >> 1) & 1u))) << 16)) |
+         ((uint64_t)nib_sel(n >> 2) << 32);
+}
 // stage-dependent layout; 1024-aligned pieces first (swizzled TMA/UMMA tiles)
 __host__ __device__ inline SmemPlan smem_plan(int bm, int stages, int ra, uint32_t rec_slot) {
   SmemPlan p;
@@ -160,10 +178,9 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t saddr, uint32_t rank) {
   uint32_t ra;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(saddr), "r"(rank));
   float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
-               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(ra)
-               : "memory");
+  // volatile: stays behind the cluster barrier (also a volatile asm); the
+  // caller issues every rank's load before the first use
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(ra));
   return v;
 }
 // acquire-release fence at GPU scope (release/acquire patterns with relaxed
@@ -372,6 +389,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                          (uint32_t)(min(kUSlice, p.K - pf * kUSlice) * 64 * p.ra * 2));
     }
   }
+  // nibble table of the decoders: static shared memory, so its address is a
+  // compile-time constant folded into the decoders' loads
+  __shared__ __align__(16) uint64_t s_lut[16];
+  if (warp == 3 && lane < 16) s_lut[lane] = nib_lut_entry(lane);
   if (warp == kWarpMma) {
     tmem_alloc(tmem_slot, 512);
     if (lane == 0) SALR_TRACE(27);
@@ -613,6 +634,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         if (!ready) mbar_wait_addr(dad, ph);
         mbar_wait_addr(dad + 8u * (uint32_t)S, ph);  // this stage's X tile (xfull)
         tc_fence_after();
+        SALR_TRACE_UNIT(6, v - u_begin);
         // next stage; probe its barrier now (the probe's round trip overlaps
         // this unit's issue)
         int s2 = s + 1;
@@ -686,6 +708,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     uint32_t ph = 0;
     for (int it = u_begin + grp; it < u_end; it += kDecGroups) {
       mbar_wait(&full[s], ph);
+      if (lane == 0 && (dw % WPG) == 0) SALR_TRACE_UNIT(1, it - u_begin);
       const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
       const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(2 * BPW * part);
       if (!(p.dbg & 1)) {
@@ -715,6 +738,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) e[j] -= c[j];
         const uint32_t vbase = smem_u32(rec) + kT2Val + 2u * goff;
+        const uint32_t lut = smem_u32(s_lut);
 #pragma unroll
         for (int pp = 0; pp < WPG / 4; ++pp) {  // this warp's part, unrolled so bands are compile-time
           if (pp != part) continue;
@@ -725,30 +749,27 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           for (int i = 0; i < 4; ++i) {
             const int b = BPW * pp + 4 * c4 + i;
             const uint32_t ev = e[(b >= 8 ? 2 : 0) + (b & 1)];
-            const uint32_t ex = (ev >> (8 * ((b & 7) >> 1))) & 0xFFu;
-            const uint32_t bov = (bo[b >> 1] >> (16 * (b & 1))) & 0xFFFFu;
-            uint32_t r = vbase + 2u * (bov + ex);
+            const uint32_t ex = prmt(ev, 0u, 0x4440u + (uint32_t)((b & 7) >> 1));
+            const uint32_t bov = prmt(bo[b >> 1], 0u, (b & 1) ? 0x4432u : 0x4410u);
+            const uint32_t r = vbase + 2u * (bov + ex);
             const uint32_t word = b < 8 ? mw.x : mw.y;
             const int sh = 4 * (b & 7);
-            // predicated pointer chain: @p ld.shared + @p add, per element
-            uint32_t v0 = 0u, v1 = 0u, v2 = 0u, v3 = 0u;
+            // nibble -> table entry (8 bytes): selectors of both words and the
+            // byte offset of word 1's first value.  Absent elements need no
+            // predicate: the selectors pick the zero bytes.
+            const uint32_t la = lut + (sh >= 3 ? ((word >> (sh - 3)) & 0x78u) : ((word << 3) & 0x78u));
+            uint32_t e0, e1, a0, a1, b0, b1;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e0), "=r"(e1) : "r"(la));
+            const uint32_t r2 = r + (e0 >> 16);
             asm volatile(
-                "{\n\t.reg .pred q0, q1, q2, q3;\n\t"
-                "setp.ne.b32 q0, %5, 0;\n\t"
-                "setp.ne.b32 q1, %6, 0;\n\t"
-                "setp.ne.b32 q2, %7, 0;\n\t"
-                "setp.ne.b32 q3, %8, 0;\n\t"
-                "@q0 ld.shared.u16 %0, [%4];\n\t"
-                "@q0 add.u32 %4, %4, 2;\n\t"
-                "@q1 ld.shared.u16 %1, [%4];\n\t"
-                "@q1 add.u32 %4, %4, 2;\n\t"
-                "@q2 ld.shared.u16 %2, [%4];\n\t"
-                "@q2 add.u32 %4, %4, 2;\n\t"
-                "@q3 ld.shared.u16 %3, [%4];\n\t}"
-                : "+r"(v0), "+r"(v1), "+r"(v2), "+r"(v3), "+r"(r)
-                : "r"(word & (1u << sh)), "r"(word & (2u << sh)), "r"(word & (4u << sh)), "r"(word & (8u << sh)));
-            packed[2 * i] = __byte_perm(v0, v1, 0x5410);
-            packed[2 * i + 1] = __byte_perm(v2, v3, 0x5410);
+                "ld.shared.u16 %0, [%4];\n\t"
+                "ld.shared.u16 %1, [%4+2];\n\t"
+                "ld.shared.u16 %2, [%5];\n\t"
+                "ld.shared.u16 %3, [%5+2];"
+                : "=r"(a0), "=r"(a1), "=r"(b0), "=r"(b1)
+                : "r"(r), "r"(r2));
+            packed[2 * i] = prmt(a0, a1, e0);
+            packed[2 * i + 1] = prmt(b0, b1, e1);
           }
           SALR_TMEM_ST_X8(taddr + 8u * c4, packed);
         }
@@ -760,8 +781,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       if (lane == 0) {
         mbar_arrive(&decoded[s]);
         if (dw == 0) SALR_TRACE(it == u_begin ? 4 : 11);
-        if (dw == 0) SALR_TRACE_UNIT(3, it - u_begin);
-        if (dw == kNumDecWarps - 1) SALR_TRACE_UNIT(4, it - u_begin);
+        if ((dw % WPG) == 0) SALR_TRACE_UNIT(3, it - u_begin);
+        if ((dw % WPG) == WPG - 1) SALR_TRACE_UNIT(4, it - u_begin);
       }
       s += kDecGroups;
       if (s >= S) { s -= S; ph ^= 1; }
@@ -1106,14 +1127,20 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     for (int e = threadIdx.x; e < (g1 - g0) * kTileN; e += kNumThreads) {
       const int nl = e % kTileN, m = 4 * (g0 + e / kTileN);
       const uint32_t a = sp + (uint32_t)((nl * (BM + 4) + m) * 4);
-      float4 acc = ld_dsmem_f4(a, 0u);
-      for (int j = 1; j < np; ++j) {
-        const float4 v = ld_dsmem_f4(a, (uint32_t)j);
-        acc.x += v.x;
-        acc.y += v.y;
-        acc.z += v.z;
-        acc.w += v.w;
-      }
+      // every remote load in flight before the (rank-ordered) sums
+      float4 v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < np) v[j] = ld_dsmem_f4(a, (uint32_t)j);
+      float4 acc = v[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j)
+        if (j < np) {
+          acc.x += v[j].x;
+          acc.y += v[j].y;
+          acc.z += v[j].z;
+          acc.w += v[j].w;
+        }
       const int n = nt * kTileN + nl;
       if (n < p.N) {
         const float o4[4] = {acc.x, acc.y, acc.z, acc.w};
@@ -1217,15 +1244,26 @@ static EncodeTiledFn get_encode_tiled() {
   return fn;
 }
 
-static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+// Host-side caches are per device ordinal: function attributes, SM counts
+// and occupancy answers belong to one device context.
+constexpr int kMaxDevices = 64;
+static int cur_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+    (void)cudaGetLastError();
+    dev = 0;
   }
-  return n;
+  return dev;
+}
+static int sm_count() {
+  static int n[kMaxDevices] = {};
+  const int dev = cur_device();
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
+  }
+  return n[dev];
 }
 
 // bf16 2-D tensor map over a row-major (rows x cols) matrix, box (64 cols, box_rows), 128B swizzle.
@@ -1259,14 +1297,14 @@ static int pick_bm(int64_t M) {
 // Deepest ring that fits shared memory and TMEM (slots sized for the largest
 // record of the matrix: ~9.6 KB at 50% sparsity instead of the 17.4 KB worst
 // case).
-static int max_stages(int bm, int ra, uint32_t rec_slot) {
+static int max_stages(int bm, int ra, uint32_t rec_slot, int cap) {
   const int acc = nacc_for(bm) * acc_cols_for(bm);
   const int tmem_stages = (512 - ((acc + 31) & ~31)) / 32;
-  // 8 slots already cover the HBM latency (measured: 12 are ~1-2 % slower
-  // on every Llama shape, 4 are 15 % slower)
-  int s = 8;
+  // default cap 8 slots (measured: 12 are ~1-2 % slower on every Llama
+  // shape, 4 are 15 % slower); an explicit request may go deeper
+  int s = cap;
   if (s > tmem_stages) s = tmem_stages;
-  while (s > 1 && smem_plan(bm, s, ra, rec_slot).total > kSmemMax) --s;
+  while (s > 1 && smem_plan(bm, s, ra, rec_slot).total > kSmemMaxLinear) --s;
   if (s > 4) s &= ~3;  // a multiple of the decoder group count
   return s;
 }
@@ -1283,10 +1321,11 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   p.base_off = plan.base_off;
   p.ad_off = plan.ad_off;
   p.bar_off = plan.bar_off;
-  static bool attr_done = false;
-  if (!attr_done) {
-    SALR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
-    attr_done = true;
+  const int dev = cur_device();
+  static bool attr_done[kMaxDevices] = {};
+  if (!attr_done[dev]) {
+    SALR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxLinear));
+    attr_done[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctas);
@@ -1314,9 +1353,14 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   if (p.cluster > 1) {
     // every cluster must be resident at once (else fall back to the global
     // split-K path); cached per configuration
-    static int64_t cached_key = -1, cached_max = 0;
+    static int64_t cached_key[kMaxDevices], cached_max[kMaxDevices];
+    static bool cached_init = false;
+    if (!cached_init) {
+      for (int d = 0; d < kMaxDevices; ++d) cached_key[d] = -1;
+      cached_init = true;
+    }
     const int64_t key = ((int64_t)p.cluster << 32) | plan.total;
-    if (key != cached_key) {
+    if (key != cached_key[dev]) {
       int n = 0;
       cudaLaunchConfig_t q = cfg;
       q.attrs = attr + (pdl ? 1 : 0);
@@ -1325,11 +1369,11 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
         (void)cudaGetLastError();
         n = 0;
       }
-      cached_key = key;
-      cached_max = n;
+      cached_key[dev] = key;
+      cached_max[dev] = n;
     }
-    cluster_max = (int)cached_max;
-    if (cached_max * p.cluster < ctas) {
+    cluster_max = (int)cached_max[dev];
+    if (cached_max[dev] * p.cluster < ctas) {
       p.cluster = 0;
       cfg.numAttrs = (unsigned)(na - 1);
     }
@@ -1376,10 +1420,11 @@ static int launch_prefill(const CUtensorMap* maps, PrefillParams pp, cudaStream_
   pp.b_off = plan.b_off;
   pp.rec_off = plan.rec_off;
   pp.bar_off = plan.bar_off;
-  static bool attr_done = false;
-  if (!attr_done) {
+  const int dev = cur_device();
+  static bool attr_done[kMaxDevices] = {};
+  if (!attr_done[dev]) {
     SALR_CUDA_TRY(cudaFuncSetAttribute(salr_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
-    attr_done = true;
+    attr_done[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)std::min<int64_t>(sm_count(), pp.items));
@@ -1514,7 +1559,7 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   {
     p.rec_slot = (max_record_bytes > 0 && max_record_bytes <= kMaxRecordBytesT2)
                      ? (uint32_t)((max_record_bytes + 15) & ~15ll) : (uint32_t)kMaxRecordBytesT2;
-    const int smax = max_stages(bm, ra, p.rec_slot);
+    const int smax = max_stages(bm, ra, p.rec_slot, stages > 8 ? std::min(stages, 16) : 8);
     p.stages = stages <= 0 || stages > smax ? smax : stages;
   }
   uint8_t* ws = static_cast<uint8_t*>(workspace);

@@ -3,6 +3,7 @@
 // no CUTLASS dependency.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -35,14 +36,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+// Suspend-time hint of the blocking waits (ns): a waiting warp is parked until
+// the phase completes or the hint elapses, so long waits cost few re-polls.
+#ifndef SALR_WAIT_HINT_NS
+#define SALR_WAIT_HINT_NS 100000
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(phase)
+      : "r"(smem_u32(bar)), "r"(phase), "n"(SALR_WAIT_HINT_NS)
       : "memory");
   return ok != 0;
 }
@@ -60,10 +66,39 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t phase) {
 }
 // Blocking wait: try_wait lets the hardware park the warp until the phase
 // completes (or a time limit), so waiting warps do not burn issue slots that
-// the decoder warps need.
+// the decoder warps need.  Debug builds (-DSALR_DEBUG) bound every wait: a
+// protocol bug traps (a launch error the host maps to SalrError) instead of
+// hanging the device -- the GPU form of the reference ring's wait timeout
+// (pipeline.py:59-60, 131-136).
+#ifdef SALR_DEBUG
+#ifndef SALR_WAIT_TIMEOUT_NS
+#define SALR_WAIT_TIMEOUT_NS 2000000000ull
+#endif
+__device__ __forceinline__ unsigned long long salr_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __noinline__ void salr_wait_timeout(uint32_t bar, uint32_t phase) {
+  printf("salr: mbarrier wait timed out (block %d thread %d, barrier 0x%x, parity %u)\n", (int)blockIdx.x,
+         (int)threadIdx.x, bar, phase);
+  __trap();
+}
+#define SALR_BOUNDED_WAIT(cond, bar, phase)                                              \
+  do {                                                                                   \
+    const unsigned long long t0_ = salr_gtimer();                                        \
+    while (!(cond)) {                                                                    \
+      if (salr_gtimer() - t0_ > SALR_WAIT_TIMEOUT_NS) salr_wait_timeout((bar), (phase)); \
+    }                                                                                    \
+  } while (0)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#ifdef SALR_DEBUG
+  SALR_BOUNDED_WAIT(mbar_try_wait(bar, phase), smem_u32(bar), phase);
+#else
   while (!mbar_try_wait(bar, phase)) {
   }
+#endif
 }
 // Spinning wait (no suspension) for very short expected waits.
 __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t phase) {
@@ -163,6 +198,17 @@ __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// 32-bit global load through L2 with a cache policy (read-only data)
+__device__ __forceinline__ uint32_t ld_u32_hint(const uint32_t* p, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 // 2-D tiled tensor copy global -> shared (box defined by the tensor map).
 __device__ __forceinline__ void tma_2d_g2s(void* dst_smem, const CUtensorMap* map, int32_t c0,
                                            int32_t c1, uint64_t* bar) {
@@ -198,6 +244,13 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
                : "memory");
+}
+// prmt.b32 (default mode): selector nibbles are used as given (the CUDA
+// __byte_perm intrinsic masks them with 0x7777 first: one more instruction)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
 }
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -282,13 +335,28 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {
 // Address-form mbarrier waits (the caller keeps barrier addresses in
 // registers and advances them incrementally).
 __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
+#ifdef SALR_DEBUG
+  auto try_once = [&]() {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(phase), "n"(SALR_WAIT_HINT_NS)
+        : "memory");
+    return ok != 0;
+  };
+  SALR_BOUNDED_WAIT(try_once(), bar, phase);
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "W_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra W_%=;\n\t}" ::"r"(bar),
-      "r"(phase)
+      "r"(phase), "n"(SALR_WAIT_HINT_NS)
       : "memory");
+#endif
 }
 __device__ __forceinline__ uint32_t mbar_test_addr(uint32_t bar, uint32_t phase) {
   uint32_t ok;

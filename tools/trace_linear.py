@@ -15,9 +15,9 @@ import torch
 import paper_2601_16991_b200 as S
 from paper_2601_16991_b200 import _lib, synthetic
 
-EV = {10: "entry", 0: "setup done", 1: "tma first", 2: "tma last", 3: "prep first", 12: "prep last",
-      4: "dec first", 11: "dec last", 5: "mma first", 6: "mma acc_full(last seg)", 7: "epi first acc",
-      8: "epi done", 9: "cta end", 19: "u start (epoch read)", 15: "u claim1 back", 16: "dec warp at setup bar", 17: "u compute1 done", 18: "u slice1 synced", 13: "u slices added", 14: "u ready seen", 20: "ticket (last split seg)", 21: "barriers init", 22: "coop0 reduced", 23: "pre-issued S units", 24: "pdl_wait done", 25: "epi seg0 stored", 26: "final syncthreads", 27: "tmem alloc done", 28: "x tiles issued", 29: "pre-ticket", 30: "ticket back", 31: "last-cta reduced"}
+EV = {10: "entry", 0: "setup done", 1: "tma first", 2: "tma last", 3: "head acc ready", 5: "head pass0 loaded", 12: "head pass0 stored",
+      4: "dec first", 11: "dec last", 6: "mma acc_full(last seg)", 7: "epi first acc",
+      8: "epi done", 9: "cta end", 19: "u start (epoch read)", 15: "u claim1 back", 16: "dec warp at setup bar", 17: "u compute1 done", 18: "u slice1 synced", 13: "u slices added", 14: "u ready seen", 20: "pub ticket added", 21: "barriers init", 22: "coop0 reduced", 23: "pre-issued S units", 24: "pdl_wait done", 25: "epi seg0 stored", 26: "final syncthreads", 27: "tmem alloc done", 28: "x tiles issued", 29: "head poll start", 30: "head ticket ok", 31: "head reduced"}
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="gate")
 ap.add_argument("--tokens", type=int, default=1)
