@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // off the arrive's latency).  The first ring's worth of units never waits
   // for `empty`.  with_x = false defers the X tile (see the PDL prologue).
   auto issue_one = [&](bool with_x) {
+    if (lane == 0) SALR_TRACE_UNIT(8, pv - u_begin);
     while (pv - chunk >= 32) {
       chunk += 32;
       co0 = no0;
@@ -302,12 +303,14 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     const uint32_t o0 = __shfl_sync(0xffffffffu, co0, pv - chunk);
     const uint32_t o1 = __shfl_sync(0xffffffffu, co1, pv - chunk);
+    if (lane == 0) SALR_TRACE_UNIT(9, pv - u_begin);
     if (pv - u_begin >= S) mbar_wait(&empty[ps], pph ^ 1);
     if (lane == 0) {
+      SALR_TRACE_UNIT(10, pv - u_begin);
       const uint32_t bytes = (p.dbg & 2) ? 0u : (o1 - o0) * 16u;
       if (bytes) bulk_g2s_hint(recbuf + (size_t)ps * p.rec_slot, p.records + (size_t)o0 * 16u, bytes, &full[ps], pol_stream);
       mbar_arrive_expect_tx(&full[ps], bytes);
-      if (with_x) issue_x(pv, ps);
+      if (with_x && !(p.dbg & 16)) issue_x(pv, ps);
       SALR_TRACE_UNIT(0, pv - u_begin);
     }
     __syncwarp();
@@ -549,7 +552,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (lane == 0 && producer) {
       const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
       const int pre = min(first_seg_end, u_begin + S);
-      for (int v = u_begin + pk; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
+      if (!(p.dbg & 16))
+        for (int v = u_begin + pk; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
     }
     __syncwarp();
     if (threadIdx.x == 0) SALR_TRACE(28);
@@ -632,7 +636,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       tc_fence_after();
       for (int v = u; v < seg_end; ++v) {
         if (!ready) mbar_wait_addr(dad, ph);
-        mbar_wait_addr(dad + 8u * (uint32_t)S, ph);  // this stage's X tile (xfull)
+        if (!(p.dbg & 16)) mbar_wait_addr(dad + 8u * (uint32_t)S, ph);  // this stage's X tile (xfull)
         tc_fence_after();
         SALR_TRACE_UNIT(6, v - u_begin);
         // next stage; probe its barrier now (the probe's round trip overlaps
@@ -738,7 +742,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #pragma unroll
         for (int j = 0; j < 4; ++j) e[j] -= c[j];
         const uint32_t vbase = smem_u32(rec) + kT2Val + 2u * goff;
-        const uint32_t lut = smem_u32(s_lut);
+        const uint8_t* const smem_base = smem_raw;
+        const uint32_t smem_base_u32 = smem_u32(smem_raw);
 #pragma unroll
         for (int pp = 0; pp < WPG / 4; ++pp) {  // this warp's part, unrolled so bands are compile-time
           if (pp != part) continue;
@@ -756,18 +761,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const int sh = 4 * (b & 7);
             // nibble -> table entry (8 bytes): selectors of both words and the
             // byte offset of word 1's first value.  Absent elements need no
-            // predicate: the selectors pick the zero bytes.
-            const uint32_t la = lut + (sh >= 3 ? ((word >> (sh - 3)) & 0x78u) : ((word << 3) & 0x78u));
-            uint32_t e0, e1, a0, a1, b0, b1;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(e0), "=r"(e1) : "r"(la));
-            const uint32_t r2 = r + (e0 >> 16);
-            asm volatile(
-                "ld.shared.u16 %0, [%4];\n\t"
-                "ld.shared.u16 %1, [%4+2];\n\t"
-                "ld.shared.u16 %2, [%5];\n\t"
-                "ld.shared.u16 %3, [%5+2];"
-                : "=r"(a0), "=r"(a1), "=r"(b0), "=r"(b1)
-                : "r"(r), "r"(r2));
+            // predicate: the selectors pick the zero bytes.  Plain (non-asm)
+            // shared loads: the compiler may overlap the bands' load chains
+            // (the mbarrier wait above is a compiler barrier for them).
+            const uint32_t nib8 = sh >= 3 ? ((word >> (sh - 3)) & 0x78u) : ((word << 3) & 0x78u);
+            const uint2 ent = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(s_lut) + nib8);
+            const uint32_t e0 = ent.x, e1 = ent.y;
+            const uint8_t* rp = smem_base + (r - smem_base_u32);
+            const uint8_t* rp2 = rp + (e0 >> 16);
+            const uint32_t a0 = *reinterpret_cast<const uint16_t*>(rp);
+            const uint32_t a1 = *reinterpret_cast<const uint16_t*>(rp + 2);
+            const uint32_t b0 = *reinterpret_cast<const uint16_t*>(rp2);
+            const uint32_t b1 = *reinterpret_cast<const uint16_t*>(rp2 + 2);
             packed[2 * i] = prmt(a0, a1, e0);
             packed[2 * i + 1] = prmt(b0, b1, e1);
           }
