@@ -111,6 +111,27 @@ int salr_tb2_count(const uint8_t* records, const uint32_t* tile_off, int64_t row
                    uint32_t* tile_off2, void* stream);
 int salr_tb2_write(const uint8_t* records, const uint32_t* tile_off, int64_t rows, int64_t cols,
                    const uint32_t* tile_off2, uint8_t* records2, void* stream);
+/* Inverse (bit-exact): bf16 TB records from TB2 records, so a matrix may keep
+ * only the compute format resident and rebuild TB on demand (decode,
+ * reference layout).  Count: tile_off[n_tiles + 1]; write: the records. */
+int salr_tb_from_tb2_count(const uint8_t* records2, const uint32_t* tile_off2, int64_t rows, int64_t cols,
+                          uint32_t* tile_off, void* stream);
+int salr_tb_from_tb2_write(const uint8_t* records2, const uint32_t* tile_off2, int64_t rows, int64_t cols,
+                          const uint32_t* tile_off, uint8_t* records, void* stream);
+
+/* ---- exact magnitude-prune masks (reference prune.py:213-255) ----------- */
+/* Global methods: mask[i] = 1 for exactly `keep` entries -- the largest
+ * scores (non-negative, float32 dtype 0 or float64 dtype 2), ties broken
+ * toward the lower flat index (the reference's stable argsort).  Radix
+ * select + ordered tie scan, stream-ordered, no host sync; workspace of
+ * salr_topk_mask_workspace_bytes(n) bytes (no initialisation needed). */
+size_t salr_topk_mask_workspace_bytes(int64_t n);
+int salr_topk_mask(const void* scores, int dtype, int64_t n, int64_t keep, uint8_t* mask, void* workspace,
+                   size_t workspace_bytes, void* stream);
+/* N:M: keep the n largest scores of every contiguous group of m columns of a
+ * row-major rows x cols matrix, ties toward the lower column offset. */
+int salr_nm_mask(const void* scores, int dtype, int64_t rows, int64_t cols, int n_keep, int m_group,
+                 uint8_t* mask, void* stream);
 
 /* ---- SALR linear forward (reference pipeline.py:405-461, fusion.py:87-130) */
 /* Y (M x N) = X (M x K) @ decode(W) + (X @ A_cat) @ B_cat.
@@ -126,12 +147,18 @@ int salr_tb2_write(const uint8_t* records, const uint32_t* tile_off, int64_t row
  *             1 = serial decode/MMA schedule, <= 0 = deepest that fits)
  *   num_ctas  persistent CTAs (<= 0: one per SM)
  *   workspace >= salr_linear_workspace_bytes(M, N, K, r_pad, num_ctas); its
- *   first 256 KiB (ticket counters at fixed offsets) must be zeroed once at
- *   allocation -- the kernels leave the counters zero
- *   on exit, so the same workspace serves back-to-back / graph-replayed
- *   calls.  Split-K partials are summed in a fixed order: results are
+ *   first salr_linear_workspace_zero_bytes() bytes (ticket counters, adapter
+ *   control words, in-kernel U accumulators at fixed offsets) must be zeroed
+ *   once at allocation -- the kernels maintain them from then on, so the same
+ *   workspace serves back-to-back / graph-replayed calls.  Split-K partials are summed in a fixed order: results are
  *   bit-identical from run to run for a given num_ctas. */
 size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pad, int num_ctas);
+/* Bytes at the start of every workspace that must be zero before its first
+ * use (ticket counters, adapter control words and the two parity buffers of
+ * the in-kernel U fixed-point accumulator; 768 KiB).  The kernels maintain
+ * the invariant from then on (counters self-reset; each launch clears the
+ * U buffer the previous launch used), so zero it once, at allocation. */
+size_t salr_linear_workspace_zero_bytes(void);
 /* Instrumentation (tools only): when buf != NULL, subsequent linear launches
  * write per-CTA %globaltimer stamps of pipeline events into buf[cta][32]
  * (u64, device memory, >= 32 * 8 * num_ctas bytes).  NULL disables. */
@@ -148,6 +175,11 @@ int salr_debug_last_launch(int32_t* info12);
  * x.  The caller must not let the preceding kernel still READ y, and must use
  * a workspace the preceding kernel does not use (alternate two). */
 #define SALR_FLAG_PDL 1
+/* flags: SALR_FLAG_U_FP32 computes U = X @ A_cat in the fp32 pre-kernel
+ * instead of the in-kernel int64 fixed-point accumulator (resolution 2^-26,
+ * range |U| < 2^37).  The Python layer sets it when the bound
+ * K * max|X| * max|A_cat| falls outside [2^-6, 2^34]. */
+#define SALR_FLAG_U_FP32 2
 int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const uint8_t* records,
                         const uint32_t* tile_off, int64_t max_record_bytes, int64_t N, const void* acat, const void* bcat_t,
                         int64_t r_pad, void* y, int y_dtype, int64_t ldy, void* workspace,

@@ -11,12 +11,16 @@ library ``libsalr_b200.so`` (no CPU fallback).
 
 from .errors import (BoundsError, ConfigError, CorruptionError, DomainError, FormatError, SalrError,
                      ShapeError, VerificationError)
-from .residual import AdapterPair
+from .linalg import SvdResult, as_matrix, matmul, matmul_call_count, reset_matmul_count, svd
+from .residual import (AdapterPair, ResidualTrainConfig, StepSizeMode, build_residual_adapter,
+                       lipschitz_constant, optimal_step_size, power_iteration_sigma_max, residual_gradient,
+                       residual_loss, train_residual, truncation_error_bound)
 from .fusion import FusedAdapters, apply_fused, apply_sequential, forward, fuse
 from .bitmap import (BitmapSparseMatrix, build_lut, bytes_per_row, compression_ratio, container_size_bytes,
                      decode, decode_block, encode, header_bytes, kept_count, popcount8, read_container,
                      write_container)
-from .pipeline import (BenchResult, PipelineConfig, PipelineProbe, SlotState, bench, pipelined_forward,
-                       pipelined_matmul, salr_linear, validate_transitions)
+from .pipeline import (BenchResult, PipelineConfig, PipelineProbe, SlotState, bench, launch_count,
+                       pipelined_forward, pipelined_matmul, reset_launch_count, salr_linear, validate_transitions)
+from .prune import PruneConfig, PruneMethod, build_mask, prune
 
 __version__ = "0.1.0"

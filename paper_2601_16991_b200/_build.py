@@ -15,7 +15,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsalr_b200.so")
-SOURCES = ["salr_codec.cu", "salr_linear.cu"]
+SOURCES = ["salr_codec.cu", "salr_linear.cu", "salr_prune.cu"]
 HEADERS = ["salr_format.cuh", "salr_ptx.cuh", "salr_status.cuh"]
 
 NVCC_FLAGS = [

@@ -17,9 +17,12 @@ from .errors import (BoundsError, ConfigError, CorruptionError, DomainError, For
                      SalrError, ShapeError)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsalr_b200.so")
-# tools/ab.sh: A/B-compare two builds of the library in one process launch
-LIB_PATH = os.environ.get("SALR_B200_LIB_AB", LIB_PATH)
+# A/B comparison of library builds (tools/ab*.sh) is a debug-build feature:
+# the release package always loads its own in-tree library.
+if os.environ.get("SALR_B200_DEBUG") == "1" and os.environ.get("SALR_B200_LIB_AB"):
+    LIB_PATH = os.environ["SALR_B200_LIB_AB"]
 
+_DEFAULT_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsalr_b200.so")
 F32, BF16, F64 = 0, 1, 2
 TILE_K, TILE_N = 64, 128
 
@@ -40,7 +43,13 @@ _SIGS = {
     "salr_from_reference_write": ([_vp, _vp, _int, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp], _int),
     "salr_tb2_count": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
     "salr_tb2_write": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp], _int),
+    "salr_tb_from_tb2_count": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
+    "salr_tb_from_tb2_write": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp], _int),
     "salr_linear_workspace_bytes": ([_i64, _i64, _i64, _i64, _int], ctypes.c_size_t),
+    "salr_linear_workspace_zero_bytes": ([], ctypes.c_size_t),
+    "salr_topk_mask_workspace_bytes": ([_i64], ctypes.c_size_t),
+    "salr_topk_mask": ([_vp, _int, _i64, _i64, _vp, _vp, ctypes.c_size_t, _vp], _int),
+    "salr_nm_mask": ([_vp, _int, _i64, _i64, _int, _int, _vp, _vp], _int),
     "salr_debug_set_trace": ([_vp], _int),
     "salr_debug_last_launch": ([_vp], _int),
     "salr_linear_forward": ([_vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _int, _i64,
@@ -64,7 +73,7 @@ def load() -> ctypes.CDLL:
                                 "(run `python -m paper_2601_16991_b200._build`)")
             lib = ctypes.CDLL(LIB_PATH)
             for name, (args, res) in _SIGS.items():
-                if "SALR_B200_LIB_AB" in os.environ and not hasattr(lib, name):
+                if LIB_PATH != _DEFAULT_LIB and not hasattr(lib, name):
                     continue  # an older build under A/B comparison
                 fn = getattr(lib, name)
                 fn.argtypes, fn.restype = args, res

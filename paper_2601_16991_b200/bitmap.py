@@ -108,8 +108,8 @@ class BitmapSparseMatrix:
         self._from_reference(bm, vals)
         if self.nnz != int(vals.numel()):
             raise CorruptionError(f"bitmap popcount {self.nnz} != values length {int(vals.numel())}")
-        self._bitmap_cache = bm
-        self._values_cache = vals if vals.dtype == torch.float32 else None
+        # the reference-layout inputs are not kept: the TB records hold the
+        # same content and .bitmap/.values rebuild it on request
 
     # ------------------------------------------------------------------ internals
     def _init_geometry(self, rows, cols, value_dtype):
@@ -117,10 +117,8 @@ class BitmapSparseMatrix:
         self.dtype_code = DTYPE_F32
         self.value_dtype = value_dtype
         self.n_kt, self.n_nt, self.n_tiles = _lib.geometry(self.rows, self.cols)
-        self._bitmap_cache = None
-        self._values_cache = None
         self._byte_starts = None
-        self._bf16 = None
+        self._tb2 = None
 
     @classmethod
     def _wrap(cls, rows, cols, value_dtype, records, tile_off):
@@ -164,30 +162,45 @@ class BitmapSparseMatrix:
 
     def _to_reference(self):
         lib = _lib.load()
-        dev = self.records.device
+        records, tile_off = self.tb()
+        dev = records.device
         bpr = bytes_per_row(self.cols)
         rowtile_off = torch.empty(self.rows * self.n_nt + 1, dtype=torch.int32, device=dev)
         bm = torch.empty((self.rows, bpr), dtype=torch.uint8, device=dev)
         vals = torch.empty(max(self.nnz, 1), dtype=torch.float32, device=dev)
-        _lib.check(lib.salr_to_reference(_lib.ptr(self.records), _u32(self.tile_off),
+        _lib.check(lib.salr_to_reference(_lib.ptr(records), _u32(tile_off),
                                          _VALUE_DTYPES[self.value_dtype][0], self.rows, self.cols, _u32(rowtile_off),
                                          _lib.ptr(bm), _lib.ptr(vals), _lib.F32, _lib.stream_ptr()))
-        self._bitmap_cache, self._values_cache = bm, vals[: self.nnz]
+        return bm, vals[: self.nnz]
+
+    def tb(self):
+        """(records, tile_off) of the TB records: the resident ones, or -- when
+        only the TB2 compute format is kept -- rebuilt from it (bit-exact,
+        transient, not cached)."""
+        if self.records is not None:
+            return self.records, self.tile_off
+        rec2, off2, _ = self._tb2
+        lib = _lib.load()
+        st = _lib.stream_ptr()
+        off = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=rec2.device)
+        _lib.check(lib.salr_tb_from_tb2_count(_lib.ptr(rec2), _u32(off2), self.rows, self.cols, _u32(off), st))
+        units = int(off[-1].item()) & 0xFFFFFFFF
+        rec = torch.empty(16 * units, dtype=torch.uint8, device=rec2.device)
+        _lib.check(lib.salr_tb_from_tb2_write(_lib.ptr(rec2), _u32(off2), self.rows, self.cols, _u32(off),
+                                              _lib.ptr(rec), st))
+        return rec, off
 
     # ------------------------------------------------------------------ reference API
     @property
     def bitmap(self) -> torch.Tensor:
-        """Reference-layout bitmap ``rows x ceil(cols/8)`` uint8 (materialised on request)."""
-        if self._bitmap_cache is None:
-            self._to_reference()
-        return self._bitmap_cache
+        """Reference-layout bitmap ``rows x ceil(cols/8)`` uint8, rebuilt on the
+        device on every access (a fresh array, like the reference's copy)."""
+        return self._to_reference()[0]
 
     @property
     def values(self) -> torch.Tensor:
-        """Values in reference row-major set-bit order, float32."""
-        if self._values_cache is None:
-            self._to_reference()
-        return self._values_cache
+        """Values in reference row-major set-bit order, float32 (fresh array)."""
+        return self._to_reference()[1]
 
     @property
     def bytes_per_row(self) -> int:
@@ -221,14 +234,30 @@ class BitmapSparseMatrix:
 
     @property
     def device_bytes(self) -> int:
-        """Actual TB bytes resident in HBM (records incl. headers/padding + offsets)."""
-        return int(self.records.numel()) + 4 * int(self.tile_off.numel())
+        """Bytes this matrix keeps resident in HBM: every stored format
+        (TB records, the TB2 compute format, offsets; cached reference
+        ``byte_starts`` if requested)."""
+        n = 0
+        if self.records is not None:
+            n += int(self.records.numel()) + 4 * int(self.tile_off.numel())
+        if self._tb2 is not None:
+            n += int(self._tb2[0].numel()) + 4 * int(self._tb2[1].numel())
+        if self._byte_starts is not None:
+            n += 8 * int(self._byte_starts.numel())
+        return n
 
     def compute_format(self):
         """(records2, tile_off2, max_record_bytes) of the TB2 compute format
-        the linear kernel consumes; built once from the bf16 TB records on the
-        current stream and cached (never inside a CUDA-graph capture)."""
-        if getattr(self, "_tb2", None) is None:
+        the linear kernel consumes; built once on the current stream and
+        cached (never inside a CUDA-graph capture).
+
+        One compute format stays resident: a bf16 matrix releases its TB
+        records once TB2 exists (``tb()`` rebuilds them bit-exactly when the
+        reference layout or a decode is requested), so a bf16 stack holds
+        ~K*N/8 + 2*nnz bytes plus the per-tile headers.  A float32 matrix
+        (reference-exact values) keeps its TB records; the bf16 records that
+        feed TB2 are transient."""
+        if self._tb2 is None:
             if torch.cuda.is_current_stream_capturing():
                 raise SalrError("build the compute format (BitmapSparseMatrix.compute_format()) before "
                                 "capturing a CUDA graph")
@@ -245,19 +274,26 @@ class BitmapSparseMatrix:
             o = off2.to(torch.int64) & 0xFFFFFFFF
             mx = int(16 * (o[1:] - o[:-1]).max().item()) if o.numel() > 1 else 0
             self._tb2 = (rec2, off2, mx)
+            del sb
+            if self.value_dtype == "bf16":
+                self.records = self.tile_off = None  # TB2 is the one resident format
         return self._tb2
 
     def to_bf16(self) -> "BitmapSparseMatrix":
-        """The same matrix with bf16 values (the linear kernel's operand format)."""
+        """The same matrix with bf16 values (the linear kernel's operand
+        format); a new object (not cached) for a float32 matrix."""
         if self.value_dtype == "bf16":
             return self
-        if self._bf16 is None:
-            self._bf16 = BitmapSparseMatrix(self.rows, self.cols, self.bitmap, self.values, value_dtype="bf16")
-        return self._bf16
+        bm, vals = self._to_reference()
+        return BitmapSparseMatrix(self.rows, self.cols, bm, vals, value_dtype="bf16")
+
+    @property
+    def device(self) -> torch.device:
+        return (self.records if self.records is not None else self._tb2[0]).device
 
     def __repr__(self):
         return (f"BitmapSparseMatrix(rows={self.rows}, cols={self.cols}, nnz={self.nnz}, "
-                f"value_dtype={self.value_dtype!r}, device={self.records.device})")
+                f"value_dtype={self.value_dtype!r}, device={self.device})")
 
 
 def encode(m, value_dtype: str = "f32") -> BitmapSparseMatrix:
@@ -294,9 +330,10 @@ def encode(m, value_dtype: str = "f32") -> BitmapSparseMatrix:
 
 
 def _decode_window(s: BitmapSparseMatrix, r0, r1, c0, c1, dtype=torch.float32) -> torch.Tensor:
-    out = torch.zeros((r1 - r0, c1 - c0), dtype=dtype, device=s.records.device)
+    out = torch.zeros((r1 - r0, c1 - c0), dtype=dtype, device=s.device)
     if r1 > r0 and c1 > c0:
-        _lib.check(_lib.load().salr_decode(_lib.ptr(s.records), _u32(s.tile_off), _VALUE_DTYPES[s.value_dtype][0],
+        records, tile_off = s.tb()
+        _lib.check(_lib.load().salr_decode(_lib.ptr(records), _u32(tile_off), _VALUE_DTYPES[s.value_dtype][0],
                                            s.rows, s.cols, r0, r1, c0, c1, _lib.ptr(out), _lib.dtype_code(dtype),
                                            c1 - c0, _lib.stream_ptr()))
     return out
@@ -319,7 +356,7 @@ def decode_block(s: BitmapSparseMatrix, row_range, byte_block_range,
     col_hi = min(8 * b1, s.cols)
     n_cols = max(col_hi - 8 * b0, 0)
     if r1 == r0 or b1 == b0 or n_cols == 0:
-        return torch.zeros((r1 - r0, n_cols), dtype=dtype, device=s.records.device)
+        return torch.zeros((r1 - r0, n_cols), dtype=dtype, device=s.device)
     return _decode_window(s, r0, r1, 8 * b0, col_hi, dtype)
 
 

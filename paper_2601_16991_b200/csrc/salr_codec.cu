@@ -436,6 +436,64 @@ __global__ void tb2_write_kernel(const uint8_t* __restrict__ records, const uint
   }
 }
 
+// TB records (16-byte units per tile) of a matrix held only in TB2 form.
+struct TbFromTb2UnitsFn {
+  const uint8_t* records2;
+  const uint32_t* tile_off2;
+  __device__ uint32_t operator()(int64_t t) const {
+    const uint32_t nnz = reinterpret_cast<const uint32_t*>(records2 + 16ull * tile_off2[t])[3];
+    return record_units(nnz, 2);
+  }
+};
+
+// Inverse of tb2_write_kernel (bit-exact): grid = n_tiles, block = 128,
+// thread n <-> tile column n.  Rebuilds the bf16 TB record of a tile from its
+// TB2 record, so a matrix can keep only the compute format resident.
+__global__ void tb_from_tb2_kernel(const uint8_t* __restrict__ records2, const uint32_t* __restrict__ tile_off2,
+                                   const uint32_t* __restrict__ tile_off, uint8_t* __restrict__ records) {
+  const int64_t t = blockIdx.x;
+  const int q = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const uint8_t* src = records2 + 16ull * tile_off2[t];
+  uint8_t* dst = records + 16ull * tile_off[t];
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(src);
+  const uint32_t goff = q ? hdr[q - 1] : 0u;
+  const uint64_t m = reinterpret_cast<const uint64_t*>(src + kT2Mask)[threadIdx.x];
+  const uint16_t* boff = reinterpret_cast<const uint16_t*>(src + kT2BandOff) + q * 16;
+  const uint32_t lt = lanemask_lt();
+  uint32_t excl[16];
+  for (int b = 0; b < 16; ++b) {
+    const uint32_t c = (uint32_t)__popcll((m >> (4 * b)) & 0xFull);
+    uint32_t incl = c;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (l >= d) incl += y;
+    }
+    excl[b] = incl - c;
+  }
+  if (threadIdx.x < 4) reinterpret_cast<uint32_t*>(dst)[threadIdx.x] = hdr[threadIdx.x];
+  uint32_t* bits = reinterpret_cast<uint32_t*>(dst + kHdrBytes) + q * kTileK;
+  const uint16_t* sv = reinterpret_cast<const uint16_t*>(src + kT2Val);
+  uint16_t* dv = reinterpret_cast<uint16_t*>(dst + kValOffset);
+  uint32_t rowpref = 0;
+  for (int r = 0; r < kTileK; ++r) {
+    const uint32_t w = __ballot_sync(0xffffffffu, (uint32_t)(m >> r) & 1u);
+    if (l == 0) bits[r] = w;
+    if ((w >> l) & 1u) {
+      const int b = r >> 2;
+      const uint32_t nib = (uint32_t)((m >> (4 * b)) & 0xFull);
+      const uint32_t rank = __popc(nib & ((1u << (r & 3)) - 1u));
+      dv[goff + rowpref + __popc(w & lt)] = sv[goff + boff[b] + excl[b] + rank];
+    }
+    rowpref += __popc(w);
+  }
+  if (threadIdx.x < 16) {
+    const uint32_t used = kValOffset + 2u * hdr[3];
+    const uint32_t end = 16u * (tile_off[t + 1] - tile_off[t]);
+    const uint32_t bpos = used + threadIdx.x;
+    if (bpos < end) dst[bpos] = 0;
+  }
+}
+
 extern "C" {
 
 int salr_version(void) { return 1; }
@@ -593,6 +651,28 @@ int salr_tb2_write(const uint8_t* records, const uint32_t* tile_off, int64_t row
   geometry(rows, cols, &n_kt, &n_nt);
   tb2_write_kernel<<<(unsigned)(n_kt * n_nt), 128, 0, static_cast<cudaStream_t>(stream)>>>(records, tile_off,
                                                                                            tile_off2, records2);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_tb_from_tb2_count(const uint8_t* records2, const uint32_t* tile_off2, int64_t rows, int64_t cols,
+                          uint32_t* tile_off, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  scan1_kernel<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(TbFromTb2UnitsFn{records2, tile_off2},
+                                                                  n_kt * n_nt, tile_off);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_tb_from_tb2_write(const uint8_t* records2, const uint32_t* tile_off2, int64_t rows, int64_t cols,
+                          const uint32_t* tile_off, uint8_t* records, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  tb_from_tb2_kernel<<<(unsigned)(n_kt * n_nt), 128, 0, static_cast<cudaStream_t>(stream)>>>(records2, tile_off2,
+                                                                                             tile_off, records);
   SALR_LAUNCH_CHECK();
   return SALR_OK;
 }

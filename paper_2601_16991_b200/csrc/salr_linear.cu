@@ -1249,6 +1249,18 @@ static EncodeTiledFn get_encode_tiled() {
   return fn;
 }
 
+// Experiment switches (environment) exist only in debug builds
+// (-DSALR_DEBUG): a release library never changes its schedule or skips work
+// because of the environment.
+static const char* dbg_env(const char* name) {
+#ifdef SALR_DEBUG
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
 // Host-side caches are per device ordinal: function attributes, SM counts
 // and occupancy answers belong to one device context.
 constexpr int kMaxDevices = 64;
@@ -1395,7 +1407,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
 static int dec_groups(int stages) {
   static int g = 0;
   if (!g) {
-    const char* e = getenv("SALR_DEC_GROUPS");
+    const char* e = dbg_env("SALR_DEC_GROUPS");
     g = e ? atoi(e) : 4;
     if (g != 1 && g != 2 && g != 4) g = 4;
   }
@@ -1508,6 +1520,8 @@ int salr_debug_last_launch(int32_t* info12) {
   return SALR_OK;
 }
 
+size_t salr_linear_workspace_zero_bytes(void) { return kUAccOff + kUAccBytes; }
+
 size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pad, int num_ctas) {
   return ws_layout(M, N, K, r_pad, num_ctas > 0 ? num_ctas : sm_count()).total;
 }
@@ -1555,7 +1569,7 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   {
     static int dbg = -1;
     if (dbg < 0) {
-      const char* e = getenv("SALR_DEBUG_MODE");
+      const char* e = dbg_env("SALR_DEBUG_MODE");
       dbg = e ? atoi(e) : 0;
     }
     p.dbg = dbg;
@@ -1590,7 +1604,7 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   // fixup for a pipeline that never fills.
   constexpr int64_t kMinUnitsPerCta = 6;
   int64_t ctas = num_ctas > 0 ? num_ctas : std::min<int64_t>(sm_count(), (p.units + kMinUnitsPerCta - 1) / kMinUnitsPerCta);
-  if (num_ctas <= 0 && M >= 16 && !(getenv("SALR_NO_ALIGNED_GRID"))) {
+  if (num_ctas <= 0 && M >= 16 && !(dbg_env("SALR_NO_ALIGNED_GRID"))) {
     // Prefer a grid (>= 6/7 of the SMs) whose per-CTA unit ranges tile the
     // K dimension exactly: every split output tile is then shared by
     // CTAs that finish together, so the split-K reduction does not wait on
@@ -1608,7 +1622,9 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   SALR_CHECK_ARG(ctas <= 65535, SALR_ERR_CONFIG, "num_ctas too large");
   // in-kernel U needs every CTA resident at once (they wait on each other's
   // partials): one CTA per SM, grid <= SM count
-  p.u_mode = ra ? ((M <= 256 && ctas <= sm_count()) ? 1 : 2) : 0;
+  // U = X A_cat in-kernel accumulates in int64 fixed point (2^-26, |U| < 2^37);
+  // SALR_FLAG_U_FP32 (inputs outside that range) selects the fp32 pre-kernel
+  p.u_mode = ra ? ((M <= 256 && ctas <= sm_count() && !(flags & SALR_FLAG_U_FP32)) ? 1 : 2) : 0;
   // cooperative split-tile reduction pays off once a partial tile has rows
   // to share (M >= 16); tiny ones stay with the last CTA (one round trip)
   p.coop = (ctas <= sm_count() && M >= 16) ? 1 : 0;
@@ -1619,7 +1635,7 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     const int64_t per = p.units / ctas;
     const int64_t np = (p.units % ctas == 0 && per < p.n_kt && p.n_kt % per == 0) ? p.n_kt / per : 0;
     const bool fits = (int64_t)p.stages * (bm * 128 + p.rec_slot) >= (int64_t)(bm + 4) * kTileN * 4;
-    static const bool no_cluster = getenv("SALR_NO_CLUSTER") != nullptr;
+    static const bool no_cluster = dbg_env("SALR_NO_CLUSTER") != nullptr;
     p.cluster = (!no_cluster && np >= 2 && np <= 8 && ctas % np == 0 && fits) ? (int)np : 0;
   }
   p.K = (int)K;
@@ -1637,7 +1653,7 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     SALR_LAUNCH_CHECK();
     pdl = true;
   }
-  static const bool no_prefill = getenv("SALR_NO_PREFILL") != nullptr;
+  static const bool no_prefill = dbg_env("SALR_NO_PREFILL") != nullptr;
   const int64_t pf_items = ((M + 128 * kPfMG - 1) / (128 * kPfMG)) * p.n_nt;
   // The prefill kernel has no split-K: it needs enough (512-token x
   // 128-column) items to occupy the GPU (measured crossover ~3/4 of the SMs).

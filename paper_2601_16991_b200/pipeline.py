@@ -25,6 +25,7 @@ all ring capacities) are bit-identical for a given CTA count.
 
 from __future__ import annotations
 
+import math
 import statistics
 from dataclasses import dataclass, field
 from enum import Enum
@@ -73,8 +74,13 @@ class PipelineConfig:
 
     @property
     def device_stages(self) -> int:
-        """Shared-memory ring slots requested from the kernel (0 = deepest)."""
-        return 1 if not self.overlap else self.ring_capacity
+        """Shared-memory ring slots requested from the kernel: 1 for the
+        serial schedule (``overlap=False``); otherwise at least the 8 slots
+        the kernel is tuned for (the reference's ``ring_capacity`` counts
+        decoded tiles in flight; the device ring holds records *and* decoded
+        tiles, and results are bit-identical for every depth).  ``salr_linear``
+        takes an explicit ``stages=`` for schedule experiments."""
+        return 1 if not self.overlap else max(self.ring_capacity, 8)
 
 
 @dataclass
@@ -144,15 +150,42 @@ def _workspace(M: int, N: int, K: int, r_pad: int, num_ctas: int, device) -> tor
     return ws
 
 
-def _prep_x(x, K: int, check_finite: bool) -> torch.Tensor:
-    xm = as_matrix(x, "x", require_finite=check_finite)
+def _prep_x(x, K: int, check_finite: bool):
+    """bf16, K padded to a multiple of 8; with ``check_finite`` also max|X|
+    (one reduction: a non-finite entry makes it non-finite) -> DomainError."""
+    xm = as_matrix(x, "x", require_finite=False)
     if xm.shape[1] != K:
         raise ShapeError(f"x cols {xm.shape[1]} != sparse rows {K}")
+    xmax = None
+    if check_finite:
+        xmax = float(xm.abs().amax())
+        if not math.isfinite(xmax):
+            raise DomainError("x contains non-finite entries")
     if xm.dtype != torch.bfloat16:
         xm = xm.to(torch.bfloat16)
     if K % 8:
         xm = torch.nn.functional.pad(xm, (0, 8 - K % 8))
-    return xm.contiguous()
+    return xm.contiguous(), xmax
+
+
+# the in-kernel U accumulator (int64 fixed point, 2^-26) is exact enough for
+# |U| bounds inside this window; outside it U comes from the fp32 pre-kernel
+_U_FIXED_MIN, _U_FIXED_MAX = 2.0 ** -6, 2.0 ** 34
+_FLAG_PDL, _FLAG_U_FP32 = 1, 2
+
+_launches = 0
+
+
+def launch_count() -> int:
+    """Kernel launches issued by :func:`salr_linear` since the last reset (one
+    fused launch per forward for M <= 256; two when U comes from the fp32
+    pre-kernel) -- the device analog of the reference's product counter."""
+    return _launches
+
+
+def reset_launch_count() -> None:
+    global _launches
+    _launches = 0
 
 
 def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *, out: torch.Tensor | None = None,
@@ -170,7 +203,7 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     if not isinstance(s, BitmapSparseMatrix):
         raise SalrError("s must be a BitmapSparseMatrix")
     rec2, off2, max_rec2 = s.compute_format()
-    xb = _prep_x(x, s.rows, check_finite)
+    xb, xmax = _prep_x(x, s.rows, check_finite)
     M = int(xb.shape[0])
     N = s.cols
     if fused is not None and (fused.d_in != s.rows or fused.d_out != s.cols):
@@ -181,9 +214,20 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
         out = torch.empty((M, N), dtype=out_dtype, device=xb.device)
     elif out.shape != (M, N) or out.dtype not in (torch.float32, torch.bfloat16) or not out.is_contiguous():
         raise ShapeError("out must be a contiguous (M, N) float32/bfloat16 tensor")
+    tail = None
+    if fused is not None and fused.total_rank > 128:
+        # the kernel's adapter operand holds 128 ranks: the rest is added by
+        # two fp32 device GEMMs after the launch (rare; the fused path covers
+        # the paper's configurations, R = 32..128)
+        fused, tail = fused.split(128)
+    flags = _FLAG_PDL if pdl else 0
     if fused is not None:
         acat, bct = fused.device_operands()
         r_pad = fused.r_pad
+        if xmax is not None:
+            bound = s.rows * xmax * fused.amax_a
+            if bound > _U_FIXED_MAX or (0.0 < bound < _U_FIXED_MIN):
+                flags |= _FLAG_U_FP32
     else:
         acat = bct = None
         r_pad = 0
@@ -191,10 +235,15 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
         ws = _workspace(M, N, s.rows, r_pad, num_ctas, xb.device)
     else:
         ws = workspace
+    global _launches
+    _launches += 1 if (fused is None or (M <= 256 and not flags & _FLAG_U_FP32)) else 2
     _lib.check(_lib.load().salr_linear_forward(
         _lib.ptr(xb), M, s.rows, int(xb.shape[1]), _lib.ptr(rec2), _lib.ptr(off2), max_rec2, N,
         _lib.ptr(acat), _lib.ptr(bct), r_pad, _lib.ptr(out), _lib.dtype_code(out.dtype), N,
-        _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), 1 if pdl else 0, _lib.stream_ptr()))
+        _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), flags, _lib.stream_ptr()))
+    if tail is not None:
+        xf = xb[:, : s.rows].float()
+        out += ((xf @ tail.a_cat.float()) @ tail.b_cat.float()).to(out.dtype)
     return out
 
 
@@ -244,7 +293,7 @@ def bench(x_shape, s: BitmapSparseMatrix, cfg: PipelineConfig, repeats: int = 5,
     b = pipelined_matmul(x, s, over)
     if not torch.equal(a, b):
         raise VerificationError("serial and overlapped outputs differ")
-    xd = _prep_x(x, s.rows, True)
+    xd, _ = _prep_x(x, s.rows, True)
 
     def timed(c):
         pipelined_matmul(xd, s, c)

@@ -64,9 +64,11 @@ def test_schedule_independence_bitwise(S):
     x = torch.randn(13, 700, generator=g)
     s = S.encode(w, value_dtype="bf16")
     ref = S.pipelined_matmul(x, s, S.PipelineConfig(overlap=False, ring_capacity=1))
-    for cap in (2, 3, 4, 8):
+    for cap in (2, 3, 4, 8, 12):
         got = S.pipelined_matmul(x, s, S.PipelineConfig(ring_capacity=cap))
         assert torch.equal(ref, got), cap
+    for st in (1, 2, 3, 4, 5, 6, 7, 8, 12, 16):  # every device ring depth
+        assert torch.equal(ref, S.salr_linear(x, s, None, stages=st)), st
     for _ in range(3):  # run-to-run determinism of the split-K fixup
         assert torch.equal(ref, S.pipelined_matmul(x, s, S.PipelineConfig()))
 

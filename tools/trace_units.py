@@ -1,7 +1,7 @@
 """Per-unit pipeline timeline of CTA 0 of the decode-size kernel (needs a
-library built with -DSALR_UNIT_TRACE; load it via SALR_B200_LIB_AB).
+library built with -DSALR_UNIT_TRACE; load it via SALR_B200_DEBUG=1 SALR_B200_LIB_AB=...).
 
-    SALR_B200_LIB_AB=ab/libT.so python tools/trace_units.py --shape gate --tokens 32
+    SALR_B200_DEBUG=1 SALR_B200_LIB_AB=ab/libT.so python tools/trace_units.py --shape gate --tokens 32
 
 Columns (us from CTA entry, SM clock / --mhz): producer issue of the record,
 decoder group sees it (full), group decode done (first / last warp), MMA warp
