@@ -108,9 +108,9 @@ struct SmemPlan {
 };
 
 // Nibble expansion table of the decoder.  For the 4-bit column mask n of a
-// 4-row band (bit i = row i present) whose values start at halfword s:
-//   word 0 (rows 0,1) = prmt(v[s],   v[s+1],   sel(n & 3))
-//   word 1 (rows 2,3) = prmt(v[s+c], v[s+c+1], sel(n >> 2)),  c = popc(n & 3)
+// 4-row band (bit i = row i present) whose values start at byte address r:
+//   word 0 (rows 0,1) = prmt(v[r],    v[r+2],    sel(n & 3))
+//   word 1 (rows 2,3) = prmt(v[r+2c], v[r+2c+2], sel(n >> 2)),  c = popc(n & 3)
 // with each v[] loaded zero-extended to 32 bits, so bytes 2,3 of the first
 // source are zero: sel(00) = 0x3232 (0), sel(01) = 0x3210 ([v, 0]),
 // sel(10) = 0x1032 ([0, v]), sel(11) = 0x5410 ([v, v']).  Entry =
@@ -394,8 +394,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   }
   // nibble table of the decoders: static shared memory, so its address is a
   // compile-time constant folded into the decoders' loads
-  __shared__ __align__(16) uint64_t s_lut[16];
+  __shared__ __align__(128) uint64_t s_lut[16];
   if (warp == 3 && lane < 16) s_lut[lane] = nib_lut_entry(lane);
+  const uint32_t lut_s = smem_u32(s_lut);
   if (warp == kWarpMma) {
     tmem_alloc(tmem_slot, 512);
     if (lane == 0) SALR_TRACE(27);
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (tmem != 0u) __trap();  // all 512 columns are ours: the MMA issuer assumes base 0
   if (threadIdx.x == 0) SALR_TRACE(0);
-  const uint32_t a_col0 = (uint32_t)((NACC * ACOLS + 31) & ~31);  // first A-stage column
+  constexpr uint32_t a_col0 = (uint32_t)((NACC * ACOLS + 31) & ~31);  // first A-stage column
 
   // ---- in-kernel U = X @ A_cat (u_mode 1): each slice partial goes into
   // the int64 fixed-point accumulator (integer atomics: order-independent,
@@ -621,10 +622,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // uniform registers.
     constexpr uint32_t kTm = 0u;
     const uint32_t atm0 = kTm + a_col0, dec0 = smem_u32(decoded), emp0 = smem_u32(empty);
+    const uint32_t xf0 = smem_u32(xfull);
     int s = 0, seg = 0;
     uint32_t ph = 0, ad_ph = 0;
-    uint32_t lo = lo0, atm = atm0, dad = dec0, ead = emp0;
-    bool ready = false;
     int u = u_begin;
     while (u < u_end) {
       const int tile_base = u - u % p.n_kt;
@@ -634,24 +634,51 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const uint32_t acc = kTm + (uint32_t)(b * ACOLS);
       mbar_wait(&acc_empty[b], acc_ph ^ 1);
       tc_fence_after();
+      if (S == 8 && !(p.dbg & 24)) {
+        // Ring of 8: the stage index is a compile-time constant in each case
+        // (Duff-style entry at the current stage), so barrier, TMEM and
+        // descriptor offsets are immediates and the per-unit loop is two
+        // barrier waits, a fence and one asm block.
+        int v = u;
+#define SALR_MMA_UNIT(K)                                                                              \
+  case K:                                                                                             \
+    if (v >= seg_end) break;                                                                          \
+    mbar_wait_addr(dec0 + 8u * (K), ph);                                                              \
+    mbar_wait_addr(xf0 + 8u * (K), ph);                                                               \
+    tc_fence_after();                                                                                 \
+    SALR_TRACE_UNIT(6, v - u_begin);                                                                  \
+    mma_ktile_ts_imm<kTm + a_col0 + 32u * (K)>(acc, lo0 + (K) * kLoStep, bhi, IDESC, v != u ? 1u : 0u, \
+                                                emp0 + 8u * (K));                                    \
+    SALR_TRACE_UNIT(5, v - u_begin);                                                                  \
+    ++v;
+        while (v < seg_end) {
+          switch (s) {
+            SALR_MMA_UNIT(0)
+            SALR_MMA_UNIT(1)
+            SALR_MMA_UNIT(2)
+            SALR_MMA_UNIT(3)
+            SALR_MMA_UNIT(4)
+            SALR_MMA_UNIT(5)
+            SALR_MMA_UNIT(6)
+            SALR_MMA_UNIT(7)
+          }
+          if (v >= seg_end) break;
+          s = 0;
+          ph ^= 1u;
+        }
+#undef SALR_MMA_UNIT
+        // stage and phase of the next unit
+        s = (seg_end - u_begin) % 8;
+        ph = (uint32_t)(((seg_end - u_begin) / 8) & 1);
+      } else {
+      int sg = s;
+      uint32_t lo = lo0 + (uint32_t)sg * kLoStep, atm = atm0 + 32u * (uint32_t)sg;
+      uint32_t dad = dec0 + 8u * (uint32_t)sg, ead = emp0 + 8u * (uint32_t)sg;
       for (int v = u; v < seg_end; ++v) {
-        if (!ready) mbar_wait_addr(dad, ph);
+        mbar_wait_addr(dad, ph);
         if (!(p.dbg & 16)) mbar_wait_addr(dad + 8u * (uint32_t)S, ph);  // this stage's X tile (xfull)
         tc_fence_after();
         SALR_TRACE_UNIT(6, v - u_begin);
-        // next stage; probe its barrier now (the probe's round trip overlaps
-        // this unit's issue)
-        int s2 = s + 1;
-        uint32_t ph2 = ph, lo2 = lo + kLoStep, atm2 = atm + 32u, dad2 = dad + 8u, ead2 = ead + 8u;
-        if (s2 == S) {
-          s2 = 0;
-          ph2 ^= 1u;
-          lo2 = lo0;
-          atm2 = atm0;
-          dad2 = dec0;
-          ead2 = emp0;
-        }
-        const bool next_ready = __any_sync(0xffffffffu, (v + 1 < u_end) && mbar_test_addr(dad2, ph2));
         if (p.dbg & 8) {  // experiment: commit without MMAs (wrong results)
           if (elect_one()) asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(ead) : "memory");
           __syncwarp();
@@ -659,13 +686,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           mma_ktile_ts(acc, atm, lo, bhi, IDESC, v != u ? 1u : 0u, ead);
         }
         SALR_TRACE_UNIT(5, v - u_begin);
-        s = s2;
-        ph = ph2;
-        lo = lo2;
-        atm = atm2;
-        dad = dad2;
-        ead = ead2;
-        ready = next_ready;
+        if (++sg == S) {
+          sg = 0;
+          ph ^= 1u;
+          lo = lo0;
+          atm = atm0;
+          dad = dec0;
+          ead = emp0;
+        } else {
+          lo += kLoStep;
+          atm += 32u;
+          dad += 8u;
+          ead += 8u;
+        }
+      }
+      s = sg;
       }
       if (u == tile_base && p.ra) {
         mbar_wait(ad_full, ad_ph);
@@ -716,17 +751,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
       const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(2 * BPW * part);
       if (!(p.dbg & 1)) {
-        const uint2 mw = *reinterpret_cast<const uint2*>(rec + kT2Mask + 8 * (32 * q + lane));
-        const uint32_t goff = q ? reinterpret_cast<const uint32_t*>(rec)[q - 1] : 0u;
-        const uint4 bo0 = *reinterpret_cast<const uint4*>(rec + kT2BandOff + 32 * q);
-        const uint4 bo1 = *reinterpret_cast<const uint4*>(rec + kT2BandOff + 32 * q + 16);
-        const uint32_t bo[8] = {bo0.x, bo0.y, bo0.z, bo0.w, bo1.x, bo1.y, bo1.z, bo1.w};
-        // band counts (4-bit fields) -> bytes: c[0] bands 0,2,4,6; c[1] 1,3,5,7;
+        const uint32_t rec_s = smem_u32(rec);
+        const uint2 mw = lds_v2_u32(rec_s + kT2Mask + 8u * (32u * q + lane));
+        // 2-bit pair counts (the first SWAR step) give c0 of every band;
+        // 4-bit band counts as bytes: c[0] bands 0,2,4,6; c[1] 1,3,5,7;
         // c[2] 8,10,12,14; c[3] 9,11,13,15
-        uint32_t nl = mw.x - ((mw.x >> 1) & 0x55555555u);
-        nl = (nl & 0x33333333u) + ((nl >> 2) & 0x33333333u);
-        uint32_t nh = mw.y - ((mw.y >> 1) & 0x55555555u);
-        nh = (nh & 0x33333333u) + ((nh >> 2) & 0x33333333u);
+        const uint32_t pl = mw.x - ((mw.x >> 1) & 0x55555555u);
+        const uint32_t ph = mw.y - ((mw.y >> 1) & 0x55555555u);
+        const uint32_t nl = (pl & 0x33333333u) + ((pl >> 2) & 0x33333333u);
+        const uint32_t nh = (ph & 0x33333333u) + ((ph >> 2) & 0x33333333u);
         const uint32_t c[4] = {nl & 0x0F0F0F0Fu, (nl >> 4) & 0x0F0F0F0Fu, nh & 0x0F0F0F0Fu, (nh >> 4) & 0x0F0F0F0Fu};
         uint32_t e[4] = {c[0], c[1], c[2], c[3]};
 #pragma unroll
@@ -741,9 +774,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) e[j] -= c[j];
-        const uint32_t vbase = smem_u32(rec) + kT2Val + 2u * goff;
-        const uint8_t* const smem_base = smem_raw;
-        const uint32_t smem_base_u32 = smem_u32(smem_raw);
+        const uint32_t goff = q ? lds_u32(rec_s + 4u * (uint32_t)(q - 1)) : 0u;
+        const uint32_t vb = rec_s + kT2Val + 2u * goff;
+        const uint4 bo0 = lds_v4_u32(rec_s + kT2BandOff + 32u * q);
+        const uint4 bo1 = lds_v4_u32(rec_s + kT2BandOff + 32u * q + 16u);
+        const uint32_t bo[8] = {bo0.x, bo0.y, bo0.z, bo0.w, bo1.x, bo1.y, bo1.z, bo1.w};
 #pragma unroll
         for (int pp = 0; pp < WPG / 4; ++pp) {  // this warp's part, unrolled so bands are compile-time
           if (pp != part) continue;
@@ -751,30 +786,33 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (int c4 = 0; c4 < BPW / 4; ++c4) {  // 4 bands -> 8 TMEM columns
           uint32_t packed[8];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int b = BPW * pp + 4 * c4 + i;
-            const uint32_t ev = e[(b >= 8 ? 2 : 0) + (b & 1)];
-            const uint32_t ex = prmt(ev, 0u, 0x4440u + (uint32_t)((b & 7) >> 1));
-            const uint32_t bov = prmt(bo[b >> 1], 0u, (b & 1) ? 0x4432u : 0x4410u);
-            const uint32_t r = vbase + 2u * (bov + ex);
-            const uint32_t word = b < 8 ? mw.x : mw.y;
-            const int sh = 4 * (b & 7);
-            // nibble -> table entry (8 bytes): selectors of both words and the
-            // byte offset of word 1's first value.  Absent elements need no
-            // predicate: the selectors pick the zero bytes.  Plain (non-asm)
-            // shared loads: the compiler may overlap the bands' load chains
-            // (the mbarrier wait above is a compiler barrier for them).
-            const uint32_t nib8 = sh >= 3 ? ((word >> (sh - 3)) & 0x78u) : ((word << 3) & 0x78u);
-            const uint2 ent = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint8_t*>(s_lut) + nib8);
-            const uint32_t e0 = ent.x, e1 = ent.y;
-            const uint8_t* rp = smem_base + (r - smem_base_u32);
-            const uint8_t* rp2 = rp + (e0 >> 16);
-            const uint32_t a0 = *reinterpret_cast<const uint16_t*>(rp);
-            const uint32_t a1 = *reinterpret_cast<const uint16_t*>(rp + 2);
-            const uint32_t b0 = *reinterpret_cast<const uint16_t*>(rp2);
-            const uint32_t b1 = *reinterpret_cast<const uint16_t*>(rp2 + 2);
-            packed[2 * i] = prmt(a0, a1, e0);
-            packed[2 * i + 1] = prmt(b0, b1, e1);
+          for (int i = 0; i < 4; i += 2) {
+            const int b = BPW * pp + 4 * c4 + i;  // bands b, b+1
+            // byte offsets of both bands' runs in 16-bit lanes: (prefix +
+            // band offset) * 2; byte prefixes are < 128, so sign-replicating
+            // selector nibbles give the zero bytes
+            const int j = (b & 7) >> 1;
+            const uint32_t pe = prmt(e[b >= 8 ? 2 : 0], e[b >= 8 ? 3 : 1],
+                                     (uint32_t)j | ((0x8u | j) << 4) | ((4u + j) << 8) | ((0x8u | j) << 12));
+            const uint32_t pr2 = pe + pe + (bo[b >> 1] + bo[b >> 1]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int bb = b + h;
+              const uint32_t r = h ? vb + (pr2 >> 16) : vb + (pr2 & 0xFFFFu);
+              const int sh = 4 * (bb & 7);
+              const uint32_t word = bb < 8 ? mw.x : mw.y;
+              // nibble -> table entry (8 bytes): selectors of both row pairs
+              // and the byte offset of pair 1's first value.  Absent elements
+              // need no predicate: the selectors pick zero bytes of the
+              // zero-extended loads.
+              const uint32_t nib8 = (sh >= 3 ? (word >> (sh - 3)) : (word << 3)) & 0x78u;
+              const uint2 ent = lds_v2_u32(lut_s | nib8);
+              const uint32_t r2 = r + (ent.x >> 16);
+              const uint32_t a0 = lds_u16z(r), a1 = lds_u16z(r + 2u);
+              const uint32_t b0 = lds_u16z(r2), b1 = lds_u16z(r2 + 2u);
+              packed[2 * (i + h)] = prmt(a0, a1, ent.x);
+              packed[2 * (i + h) + 1] = prmt(b0, b1, ent.y);
+            }
           }
           SALR_TMEM_ST_X8(taddr + 8u * c4, packed);
         }

@@ -93,7 +93,10 @@ __device__ __noinline__ void salr_wait_timeout(uint32_t bar, uint32_t phase) {
   } while (0)
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-#ifdef SALR_DEBUG
+#if defined(SALR_WAIT_SPIN)
+  while (!mbar_test_wait(bar, phase)) {
+  }
+#elif defined(SALR_DEBUG)
   SALR_BOUNDED_WAIT(mbar_try_wait(bar, phase), smem_u32(bar), phase);
 #else
   while (!mbar_try_wait(bar, phase)) {
@@ -252,6 +255,40 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
   asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
   return d;
 }
+// Shared-memory loads by 32-bit shared address (the decoders keep record
+// addresses as shared-window offsets; "memory" keeps them behind the
+// mbarrier waits that publish the data).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16z(uint32_t a) {  // zero-extended
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 lds_v2_u32(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4_u32(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
+// Funnel shifts of the 64-bit {hi:lo} right by n (wrap: n mod 32; clamp: min(n, 32)).
+__device__ __forceinline__ uint32_t shf_r_wrap(uint32_t lo, uint32_t hi, uint32_t n) {
+  uint32_t d;
+  asm("shf.r.wrap.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(n));
+  return d;
+}
+__device__ __forceinline__ uint32_t shf_r_clamp(uint32_t lo, uint32_t hi, uint32_t n) {
+  uint32_t d;
+  asm("shf.r.clamp.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(lo), "r"(hi), "r"(n));
+  return d;
+}
 __device__ __forceinline__ void tc_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -335,7 +372,15 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {
 // Address-form mbarrier waits (the caller keeps barrier addresses in
 // registers and advances them incrementally).
 __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
-#ifdef SALR_DEBUG
+#if defined(SALR_WAIT_SPIN)
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W_%=;\n\t}" ::"r"(bar),
+      "r"(phase)
+      : "memory");
+#elif defined(SALR_DEBUG)
   auto try_once = [&]() {
     uint32_t ok;
     asm volatile(
@@ -400,6 +445,37 @@ __device__ __forceinline__ void mma_ktile_ts(uint32_t d_tm, uint32_t a_tm, uint3
       "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], d3, %5, pt;\n\t"
       "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%6];\n\t}" ::"r"(d_tm),
       "r"(a_tm), "r"(lo), "r"(hi), "r"(accumulate), "r"(idesc), "r"(empty_bar)
+      : "memory");
+}
+
+// Same k-tile with compile-time TMEM operand addresses (A = kA.., D = d_tm)
+// and the X descriptor low word in a register: the stage index of the
+// caller is a template constant, so the only runtime operands are the
+// descriptor base, the accumulate flag and the barrier.
+template <uint32_t kA>
+__device__ __forceinline__ void mma_ktile_ts_imm(uint32_t d_tm, uint32_t lo, uint32_t hi, uint32_t idesc,
+                                                 uint32_t accumulate, uint32_t empty_bar) {
+  asm volatile(
+      "{\n\t.reg .pred pe, pa, pt;\n\t"
+      ".reg .b32 l1, l2, l3;\n\t"
+      ".reg .b64 d0, d1, d2, d3;\n\t"
+      "elect.sync _|pe, 0xffffffff;\n\t"
+      "setp.ne.b32 pa, %3, 0;\n\t"
+      "setp.eq.b32 pt, 0, 0;\n\t"
+      "add.u32 l1, %1, 2;\n\t"
+      "add.u32 l2, %1, 4;\n\t"
+      "add.u32 l3, %1, 6;\n\t"
+      "mov.b64 d0, {%1, %2};\n\t"
+      "mov.b64 d1, {l1, %2};\n\t"
+      "mov.b64 d2, {l2, %2};\n\t"
+      "mov.b64 d3, {l3, %2};\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], d0, %4, pa;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], d1, %4, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], d2, %4, pt;\n\t"
+      "@pe tcgen05.mma.cta_group::1.kind::f16 [%0], [%9], d3, %4, pt;\n\t"
+      "@pe tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%5];\n\t}" ::"r"(d_tm),
+      "r"(lo), "r"(hi), "r"(accumulate), "r"(idesc), "r"(empty_bar), "r"(kA), "r"(kA + 8), "r"(kA + 16),
+      "r"(kA + 24)
       : "memory");
 }
 

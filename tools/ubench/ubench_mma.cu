@@ -54,6 +54,21 @@ __global__ void ubench(long long* out) {
     mbar_wait(&bar[1], (R - 1) & 1);
     t1 = clock64();
     out[3] = t1 - t0;
+    // ts without per-unit commit (one commit at the end)
+    t0 = clock64();
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) mma_ts(tmem, tmem + 256 + 8 * j, bdesc + 2 * j, IDESC, 1u);
+    }
+    tc_commit(&bar[3]);
+    t1 = clock64();
+    out[5] = (t1 - t0) / R;
+    // commit only
+    t0 = clock64();
+    for (int r = 0; r < R; ++r) tc_commit(&bar[3]);
+    t1 = clock64();
+    out[6] = (t1 - t0) / R;
+    out[7] = 0;
     // serial: unit = 4 mma + commit + wait for completion (latency per unit)
     t0 = clock64();
     for (int r = 0; r < 16; ++r) {
@@ -84,8 +99,8 @@ int main() {
     ubench<16><<<1, 128, 70000>>>(out);
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(h, out, 8 * 8, cudaMemcpyDeviceToHost);
-    printf("N=16 err=%d: ts unit issue %lld, drain %lld | ss unit issue %lld, drain %lld | serial unit %lld cycles\n",
-           (int)e, h[0], h[1], h[2], h[3], h[4]);
+    printf("N=16 err=%d: ts unit issue %lld, drain %lld | ss unit issue %lld, drain %lld | serial unit %lld cycles | 4mma no commit %lld | commit %lld | ktile_ts %lld\n",
+           (int)e, h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7]);
     ubench<32><<<1, 128, 70000>>>(out);
     e = cudaDeviceSynchronize();
     cudaMemcpy(h, out, 8 * 8, cudaMemcpyDeviceToHost);
