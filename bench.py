@@ -17,10 +17,13 @@ measured HBM copy bandwidth), cuBLAS dense-bf16 comparator, clocks (NVML
 sampled during the timed region), and the CPU baseline (oracle port of the
 reference pipelined_forward on the host cores, bounded sample).
 
-``--impl reference`` times the reference's CPU algorithm instead (the oracle
-port in oracle/salr_oracle.py; the reference package itself is pure Python
-and cannot travel to the GPU box) on the same workload and prints the same
-metric with "impl": "reference".
+``--impl reference`` times the reference's own CPU implementation instead:
+the unmodified package installed offline into baseline/_ref (pure
+Python/NumPy, its stock ``salr.pipeline.pipelined_forward``), on layer 0 of
+the same stack (the same seeded weights, adapters and X as the GPU arm), one
+layer per step, and prints the same metric with "impl": "reference".  Only
+when baseline/_ref is missing does it fall back to the oracle port
+(oracle/salr_oracle.py, kind "port").
 """
 
 from __future__ import annotations
@@ -162,70 +165,87 @@ def _reference_pkg():
         return None
 
 
-def cpu_sample(tokens: int, sparsity: float, budget_s: float = 20.0, prefer_reference: bool = True):
-    """Time the reference CPU path of one layer's 7 linears at M=tokens (a
-    bounded sample of the stack workload; x32 layers extrapolated).
-
-    Prefers the real reference package (``salr.pipeline.pipelined_forward``
-    with its stock ``PipelineConfig()``, from baseline/_ref, kind
-    "reference"); falls back to the oracle port (oracle/salr_oracle.py, kind
-    "port") when baseline/_ref is absent."""
-    import numpy as np
-    from paper_2601_16991_b200 import synthetic
-
+def _blas_threads():
     try:
         from threadpoolctl import threadpool_info
-        blas_threads = max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
+        return max((i.get("num_threads", 1) for i in threadpool_info()), default=1)
     except Exception:
-        blas_threads = os.cpu_count()
-    ref = _reference_pkg() if prefer_reference else None
-    rng = np.random.default_rng(0)
-    x = synthetic.gen_x(tokens, 14336, seed=7).double().numpy()
-    q = {0.3: 0.3853204664075676, 0.5: 0.6744897501960817, 0.7: 1.0364333894937898}[sparsity]
-    linears = {}
-    for i, name in enumerate(LINEARS):
-        k, n = SHAPES[name]
-        w = synthetic.gen_weight(k, n, 1000 + i).double().numpy()
-        w[np.abs(w) < 0.02 * q] = 0.0  # magnitude prune at the N(0, 0.02^2) quantile
-        a = [rng.normal(size=(k, 16)) / 64, rng.normal(size=(k, 16)) / 64]
-        b = [rng.normal(size=(16, n)) * 0.02, rng.normal(size=(16, n)) * 0.02]
-        if ref is not None:
-            bitmap, fusion, pipeline, residual = ref
-            s = bitmap.encode(w)
-            ads = [residual.AdapterPair(a[0], b[0], 16), residual.AdapterPair(a[1], b[1], 16, 2.0)]
-            linears[name] = (s, fusion.fuse(ads), k)
-        else:
-            from oracle import salr_oracle as O
-            s = O.encode(w)
-            ads = [O.Adapter(a[0], b[0], 16), O.Adapter(a[1], b[1], 16, 2.0)]
-            linears[name] = (s, O.fuse(ads), k)
+        return os.cpu_count()
+
+
+class RefLayer:
+    """Layer 0 of the bench stack prepared for the reference CPU path: the
+    GPU arm's own seeded weights / adapters / X (generated with the same
+    seeds on the GPU when one is present, then copied to host float64),
+    encoded and fused by the reference package itself (baseline/_ref), or by
+    the oracle port when that is absent."""
+
+    def __init__(self, tokens, sparsity):
+        import torch
+        dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+        self.rng_device = dev.type
+        layer = gen_layer(0, 1, 0, sparsity, dev)
+        self.x = gen_x(tokens, dev).double().cpu().numpy()
+        self.ref = _reference_pkg()
+        self.kind = "reference" if self.ref is not None else "port"
+        self.linears = []
+        self.comp = 0
+        for name in STACK_ORDER:
+            w, ads, (k, n), _ = layer[name]
+            wn = w.double().cpu().numpy()
+            if self.ref is not None:
+                bitmap, fusion, pipeline, residual = self.ref
+                sm = bitmap.encode(wn)
+                fz = fusion.fuse([residual.AdapterPair(a.double().cpu().numpy(), b.double().cpu().numpy(), 16, sc)
+                                  for a, b, sc in ads])
+            else:
+                from oracle import salr_oracle as O
+                sm = O.encode(wn)
+                fz = O.fuse([O.Adapter(a.double().cpu().numpy(), b.double().cpu().numpy(), 16, sc)
+                             for a, b, sc in ads])
+            self.linears.append((name, sm, fz, k))
+            self.comp += sm.rows * ((sm.cols + 7) // 8) + 2 * sm.nnz  # algorithmic bytes, bf16 values
+        del layer
+
+    def forward(self, overlap=True):
+        """One layer (q|k|v, o, gate|up, down) at M tokens through the stock
+        reference pipelined_forward; o consumes the q columns and down the
+        gate columns, as on the GPU."""
+        h = self.x
+        for name, sm, fz, k in self.linears:
+            if self.ref is not None:
+                pipeline = self.ref[2]
+                y = pipeline.pipelined_forward(h[:, :k], sm, fz, pipeline.PipelineConfig(overlap=overlap))
+            else:
+                from oracle import salr_oracle as O
+                y = O.pipelined_forward(h[:, :k], sm, fz)
+            h = y
+        return h
+
+
+def cpu_sample(tokens: int, sparsity: float, budget_s: float = 20.0):
+    """Bounded CPU baseline for the GPU arm's line: median of up to 3 passes
+    of layer 0 through the reference path (stock overlap=True), x32 layers."""
+    rl = RefLayer(tokens, sparsity)
     times = []
     t_start = time.perf_counter()
     while True:
         t0 = time.perf_counter()
-        for name in LINEARS:
-            s, f, k = linears[name]
-            if ref is not None:
-                ref[2].pipelined_forward(x[:, :k], s, f, ref[2].PipelineConfig())
-            else:
-                from oracle import salr_oracle as O
-                O.pipelined_forward(x[:, :k], s, f)
+        rl.forward()
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_start > budget_s or len(times) >= 3:
             break
     layer_s = statistics.median(times)
     step_s = layer_s * 32
-    comp = sum(linears[nm][0].rows * ((linears[nm][0].cols + 7) // 8) + 4 * linears[nm][0].nnz for nm in LINEARS)
-    what = ("reference salr.pipeline.pipelined_forward (stock PipelineConfig(): 64x8-byte tiles, decoder "
-            "thread + ring, f64) from baseline/_ref" if ref is not None else
+    what = ("reference salr.pipeline.pipelined_forward (stock PipelineConfig(): overlap=True, decoder "
+            "thread + ring, f64) from baseline/_ref" if rl.kind == "reference" else
             "oracle port of pipelined_forward (f64, 64x8-byte tiles, serial)")
     return {
-        "value": tokens / step_s, "unit": "tokens/s", "cores": blas_threads,
-        "kind": "reference" if ref is not None else "port",
-        "sample": f"{what} over one layer's 7 linears at M={tokens}, median of {len(times)} passes = "
-                  f"{layer_s:.3f} s/layer, x32 layers extrapolated; {os.cpu_count()} host cores visible, "
-                  f"OpenBLAS threads={blas_threads}",
-        "compressed_gbs": comp * 32 / step_s / 1e9,
+        "value": tokens / step_s, "unit": "tokens/s", "cores": _blas_threads(), "kind": rl.kind,
+        "sample": f"{what} over layer 0 of the bench stack (the same seeded weights as the GPU arm; 4 linears: "
+                  f"q|k|v, o, gate|up, down) at M={tokens}, median of {len(times)} passes = {layer_s:.3f} s/layer, "
+                  f"x32 layers; {os.cpu_count()} host cores visible, OpenBLAS threads={_blas_threads()}",
+        "compressed_gbs": rl.comp * 32 / step_s / 1e9,
         "layer_s": layer_s,
     }
 
@@ -240,23 +260,46 @@ def stack_config(args, world, how):
 
 
 def run_reference(args):
+    """Reference arm: the reference's own CPU implementation (baseline/_ref)
+    on layer 0 of the same stack.  One step = one of the 32 identical-shape
+    layers (4 linears); value = M / (32 x step time) tokens/s of the stack.
+    Exactly --steps timed steps after --warmup untimed ones (all with the
+    stock overlap=True configuration); overlap=False is timed once more after
+    the timed region and reported beside it."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    res = cpu_sample(args.tokens, args.sparsity)
-    steps_s = []
-    for _ in range(max(1, min(args.steps, 1))):
-        steps_s.append(32 * res["layer_s"])
-    ms = 1e3 * statistics.median(steps_s)
+    rl = RefLayer(args.tokens, args.sparsity)
+    for _ in range(args.warmup):
+        rl.forward()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rl.forward()
+    total = time.perf_counter() - t0
+    layer_s = total / args.steps
+    t1 = time.perf_counter()
+    rl.forward(overlap=False)
+    serial_s = time.perf_counter() - t1
+    value = args.tokens / (32 * layer_s)
+    cores = _blas_threads()
+    what = ("reference salr.pipeline.pipelined_forward from baseline/_ref (unmodified)" if rl.kind == "reference"
+            else "oracle port of pipelined_forward (baseline/_ref missing)")
     line = {
-        "metric": METRIC, "impl": "reference", "value": res["value"], "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * layer_s, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": stack_config(args, world, "CPU (reference host path)"),
-        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
-        "e2e": {"value": res["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "compressed_gbs": res["compressed_gbs"],
+        "config": dict(stack_config(args, world, "CPU (reference host path)"),
+                       step="one of the 32 layers (q|k|v, o, gate|up, down at M tokens); value = M / (32 x step)",
+                       weights=f"layer 0 of the GPU arm (same seeds; generated on {rl.rng_device})"),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": rl.kind,
+                         "sample": f"{what}, stock PipelineConfig() (overlap=True), {args.steps} timed layers "
+                                   f"after {args.warmup} warm-up layers; {os.cpu_count()} host cores, "
+                                   f"OpenBLAS threads={cores}"},
+        "overlap_false": {"value": args.tokens / (32 * serial_s), "unit": "tokens/s", "ms_per_layer": 1e3 * serial_s,
+                          "note": "PipelineConfig(overlap=False), one layer after the timed region"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "compressed_gbs": rl.comp / layer_s / 1e9,
     }
     print(json.dumps(line), flush=True)
 
@@ -276,45 +319,92 @@ FUSED = {"qkv": (4096, [("q", 4096), ("k", 1024), ("v", 1024)]),
 STACK_ORDER = ("qkv", "o", "gateup", "down")
 
 
-def build_stack(layers, world, rank, sparsity, device):
-    """Per layer: {fused name: (BitmapSparseMatrix shard, FusedAdapters shard, (k, n_local), col range)}."""
-    import torch
-    import paper_2601_16991_b200 as S
-
-    g = torch.Generator(device=device).manual_seed(1234 + 17 * rank)
+def _prune_threshold(sparsity):
     q = {0.3: 0.3853204664075676, 0.5: 0.6744897501960817, 0.7: 1.0364333894937898}.get(sparsity)
     if q is None:
         raise SystemExit(f"unsupported sparsity {sparsity}")
-    thr = 0.02 * q  # |w| quantile of N(0, 0.02^2): magnitude pruning at `sparsity`
+    return 0.02 * q  # |w| quantile of N(0, 0.02^2): magnitude pruning at `sparsity`
+
+
+def gen_layer(layer, world, rank, sparsity, device):
+    """Dense inputs of one stack layer, seeded per (layer, rank) so any layer
+    can be regenerated alone: {fused name: (W_hat bf16 (k x n_local),
+    [(A, B, scale)] bf16-exact fp32 adapter factors, (k, n_local), (c0, c1))}.
+    The reference arm regenerates layer 0 with the same seeds."""
+    import torch
+    g = torch.Generator(device=device).manual_seed(1234 + 7919 * layer + 17 * rank)
+    thr = _prune_threshold(sparsity)
+    out = {}
+    for name in STACK_ORDER:
+        k, parts = FUSED[name]
+        n = sum(w for _, w in parts)
+        c0, c1 = shard_cols(n, world, rank)
+        nl = c1 - c0
+        w = (torch.randn(k, nl, generator=g, device=device) * 0.02).to(torch.bfloat16)
+        w = torch.where(w.float().abs() < thr, torch.zeros_like(w), w)
+        ads = []
+        p0 = 0
+        for _, pw in parts:  # LoRA r16 + residual r16 per original linear, on its own columns
+            lo, hi = max(p0, c0) - c0, min(p0 + pw, c1) - c0
+            for scale in (1.0, 2.0):
+                a = (torch.randn(k, 16, generator=g, device=device) / 64).bfloat16().float()
+                bm = torch.zeros(16, nl, device=device)
+                if hi > lo:
+                    bm[:, lo:hi] = (torch.randn(16, hi - lo, generator=g, device=device) * 0.02).bfloat16().float()
+                ads.append((a, bm, scale))
+            p0 += pw
+        out[name] = (w, ads, (k, nl), (c0, c1))
+    return out
+
+
+def gen_x(tokens, device):
+    import torch
+    g = torch.Generator(device=device).manual_seed(7)
+    return torch.randn(tokens, 4096, generator=g, device=device).bfloat16()
+
+
+def build_stack(layers, world, rank, sparsity, device):
+    """Per layer: {fused name: (BitmapSparseMatrix shard, FusedAdapters shard, (k, n_local), col range)}."""
+    import paper_2601_16991_b200 as S
+
     stack = []
     for layer in range(layers):
         lin = {}
-        for name in STACK_ORDER:
-            k, parts = FUSED[name]
-            n = sum(w for _, w in parts)
-            c0, c1 = shard_cols(n, world, rank)
-            nl = c1 - c0
-            w = (torch.randn(k, nl, generator=g, device=device) * 0.02).to(torch.bfloat16)
-            w = torch.where(w.float().abs() < thr, torch.zeros_like(w), w)
+        for name, (w, ads, kn, cols) in gen_layer(layer, world, rank, sparsity, device).items():
             s = S.encode(w, value_dtype="bf16")
             s.compute_format()  # the linear kernel's operand format, built once at load
             del w
-            ads = []
-            p0 = 0
-            for _, pw in parts:  # LoRA r16 + residual r16 per original linear, on its own columns
-                lo, hi = max(p0, c0) - c0, min(p0 + pw, c1) - c0
-                for scale in (1.0, 2.0):
-                    a = (torch.randn(k, 16, generator=g, device=device) / 64).bfloat16().float()
-                    bm = torch.zeros(16, nl, device=device)
-                    if hi > lo:
-                        bm[:, lo:hi] = (torch.randn(16, hi - lo, generator=g, device=device) * 0.02).bfloat16().float()
-                    ads.append(S.AdapterPair(a, bm, 16, scale))
-                p0 += pw
-            fused = S.fuse(ads)
+            fused = S.fuse([S.AdapterPair(a, b, 16, sc) for a, b, sc in ads])
             fused.device_operands()
-            lin[name] = (s, fused, (k, nl), (c0, c1))
+            lin[name] = (s, fused, kn, cols)
         stack.append(lin)
     return stack
+
+
+def layer_check(lin, x, layer0):
+    """End-of-run parity check: the 4 fused linears of one layer through the
+    product path vs a float64 dense reference on the same bf16-exact inputs
+    (X, W_hat, A, B): rel-Frobenius and max-abs of each output."""
+    import torch
+    import paper_2601_16991_b200 as S
+    worst = {"rel_frob": 0.0, "max_abs_rel": 0.0}
+    h = x
+    for name in STACK_ORDER:
+        s, f, (k, nl), _ = lin[name]
+        w, ads, _, _ = layer0[name]
+        xin = h[:, :k]
+        y = S.salr_linear(xin, s, f, out_dtype=torch.float32, check_finite=False).double()
+        ref = xin.double() @ w.double()
+        for a, b, sc in ads:
+            ref += sc * ((xin.double() @ a.double()) @ b.double())
+        rel = float((y - ref).norm() / ref.norm())
+        mabs = float((y - ref).abs().max() / ref.abs().max())
+        worst["rel_frob"] = max(worst["rel_frob"], rel)
+        worst["max_abs_rel"] = max(worst["max_abs_rel"], mabs)
+        h = y.bfloat16()
+    worst["tolerance"] = "rel_frob <= 5e-4 and max_abs <= 2.5e-4 * max|ref| (fp32 accumulate, bf16 operands)"
+    worst["ok"] = worst["rel_frob"] <= 5e-4 and worst["max_abs_rel"] <= 2.5e-4
+    return worst
 
 
 class StackRunner:
@@ -469,7 +559,7 @@ def run_salr(args):
 
     # ---- device-timed steps (graph-captured stack)
     runner = StackRunner(stack, M, world, torch.bfloat16)
-    x0 = torch.randn(M, 4096, device=dev).bfloat16()
+    x0 = gen_x(M, dev)
     runner.x_in.copy_(x0)
     use_graph = world == 1
     if use_graph:
@@ -528,15 +618,23 @@ def run_salr(args):
         k_bytes = sum(v["compressed_bytes"] for v in per.values())
         k_us = sum(v["us"] for v in per.values())
         achieved = k_bytes / (k_us * 1e-6) / 1e9
-        traffic = None
+        # DRAM bytes of the dominant launch (gate|up, the largest share of the
+        # step) from one committed `ncu --set full` capture of the same launch
+        # (tools/gpu_ncu_bench.sh); null when that capture is absent
+        traffic, traffic_src = None, None
         prof = os.path.join(REPO, "profiles", "ncu_summary.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("traffic_bytes_per_launch")
+                d = json.load(open(prof))
+                if d.get("launch") == f"gateup M={M}":
+                    traffic, traffic_src = d.get("traffic_bytes_per_launch"), d.get("source")
             except Exception:
                 traffic = None
+        dom = max(per, key=lambda n: per[n]["us"])
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                "frac": achieved / hbm_peak, "traffic": traffic, "traffic_source": traffic_src,
+                "traffic_algorithmic_bytes": per["gateup"]["compressed_bytes"],
+                "dominant_launch": dom, "peak_source": peak_src,
                 "kernel": "salr_linear_kernel (+ adapter_u_kernel, PDL-overlapped)",
                 "algorithmic_bytes": "K*ceil(N/8) + 2*nnz per linear (SURVEY.md 8(d))",
                 "per_linear": per}
@@ -550,7 +648,8 @@ def run_salr(args):
         if world == 1:
             for mb in [int(v) for v in args.batches.split(",") if v]:
                 if mb == M:
-                    per_m[str(mb)] = {"tokens_per_s": tokens_per_s, "ms_per_step": ms_per_step}
+                    per_m[str(mb)] = {"tokens_per_s": tokens_per_s, "ms_per_step": ms_per_step, "clocks": clocks,
+                                      "compressed_gbs": comp_bytes / (ms_per_step / 1e3) / 1e9}
                     continue
                 r2 = StackRunner(stack, mb, 1, torch.bfloat16)
                 r2.x_in.copy_(torch.randn(mb, 4096, device=dev).bfloat16())
@@ -559,11 +658,18 @@ def run_salr(args):
                 g2 = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g2):
                     r2.step(r2.x_in)
-                ms2, _ = time_steps(g2.replay, max(5, args.steps // 2), 3, 1, local)
-                per_m[str(mb)] = {"tokens_per_s": mb / (ms2 / max(5, args.steps // 2) / 1e3),
+                ms2, clk2 = time_steps(g2.replay, max(5, args.steps // 2), 3, 1, local)
+                per_m[str(mb)] = {"clocks": clk2, "tokens_per_s": mb / (ms2 / max(5, args.steps // 2) / 1e3),
                                   "ms_per_step": ms2 / max(5, args.steps // 2),
                                   "compressed_gbs": comp_bytes / (ms2 / max(5, args.steps // 2) / 1e3) / 1e9}
                 del g2, r2
+        resident = sum(lin[n][0].device_bytes for lin in stack for n in STACK_ORDER)
+        dense_bf16 = sum(2 * lin[n][2][0] * lin[n][2][1] for lin in stack for n in STACK_ORDER)
+        memory = {"resident_weight_bytes": resident, "dense_bf16_bytes": dense_bf16,
+                  "compression_vs_dense_bf16": dense_bf16 / resident,
+                  "resident_bytes_per_weight": resident / (dense_bf16 / 2),
+                  "format": "TB2 records + tile offsets only (the compute format; TB rebuilt on demand)"}
+        check = layer_check(stack[0], x0, gen_layer(0, world, rank, args.sparsity, dev))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             c = cpu_sample(M, args.sparsity)
@@ -583,6 +689,8 @@ def run_salr(args):
                            "device Y -> pinned host, synchronize; wall clock"},
             "gpu_launches": runner.launches_per_step * args.steps,
             "clocks": clocks,
+            "memory": memory,
+            "check": check,
             "per_batch": per_m,
             "setup_s": setup_s,
             **extra,

@@ -167,13 +167,20 @@ int salr_debug_set_trace(void* buf);
  * salr_linear_forward launch on this host thread's process: {ctas, stages,
  * BM, decoder groups, u_mode (0 none, 1 in-kernel U, 2 U pre-kernel), coop,
  * cluster size (0 = global split-K reduction), pdl, cluster size requested,
- * max co-resident clusters (-1 = not queried), dynamic smem bytes, 0}. */
+ * max co-resident clusters (-1 = not queried), dynamic smem bytes,
+ * cooperative (1 = launched co-scheduled: in-kernel U / cooperative split-K
+ * wait on other CTAs, so the driver guarantees every CTA is resident)}. */
 int salr_debug_last_launch(int32_t* info12);
 /* flags: SALR_FLAG_PDL launches the kernel as a programmatic dependent of the
  * preceding work on the stream: its weight-streaming prologue overlaps the
  * tail of that work and it waits for it (griddepcontrol.wait) before reading
  * x.  The caller must not let the preceding kernel still READ y, and must use
- * a workspace the preceding kernel does not use (alternate two). */
+ * a workspace the preceding kernel does not use (alternate two).  Without the
+ * flag, launches whose CTAs wait on each other (in-kernel U, cooperative
+ * split-K) are co-scheduled (cooperative launch: the driver guarantees every
+ * CTA resident).  With it they are not (co-scheduling would wait for the
+ * preceding grid to drain): the grid is checked against occupancy, and the
+ * caller must not run concurrent kernels that wait on this grid. */
 #define SALR_FLAG_PDL 1
 /* flags: SALR_FLAG_U_FP32 computes U = X @ A_cat in the fp32 pre-kernel
  * instead of the in-kernel int64 fixed-point accumulator (resolution 2^-26,

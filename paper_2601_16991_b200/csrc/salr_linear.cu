@@ -1387,7 +1387,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   cfg.blockDim = dim3(kNumThreads);
   cfg.dynamicSmemBytes = plan.total;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
   if (pdl) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1433,9 +1433,52 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
       cfg.numAttrs = (unsigned)(na - 1);
     }
   }
-  SALR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p));
+  // In-kernel U (u_mode 1) and the cooperative split-K reduction wait on
+  // other CTAs of the grid: forward progress needs every CTA resident at
+  // once.  A cooperative launch makes the driver guarantee that (or fail
+  // the launch) instead of relying on grid <= SM count alone, so a
+  // concurrent kernel (an NCCL collective on another stream, MPS) cannot
+  // deadlock the spinning CTAs.  A programmatic-dependent launch (flag
+  // SALR_FLAG_PDL, chained kernels of one stream) is not co-scheduled --
+  // co-scheduling would wait for the preceding grid to drain and void the
+  // overlap -- so it is checked against occupancy instead, and the PDL
+  // contract (include/salr_b200.h) excludes concurrent kernels that wait on
+  // this grid.
+  int coop_launch = 0;
+  if ((p.u_mode == 1 || p.coop) && pdl) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNumThreads, plan.total) != cudaSuccess) {
+      (void)cudaGetLastError();
+      per_sm = 1;
+    }
+    SALR_CHECK_ARG((int64_t)per_sm * sm_count() >= ctas, SALR_ERR_CUDA,
+                   "grid of %d CTAs cannot be co-resident (%d per SM)", ctas, per_sm);
+  }
+  if ((p.u_mode == 1 || p.coop) && !pdl) {
+    attr[cfg.numAttrs].id = cudaLaunchAttributeCooperative;
+    attr[cfg.numAttrs].val.cooperative = 1;
+    cfg.numAttrs += 1;
+    coop_launch = 1;
+  }
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p);
+  if (le != cudaSuccess && coop_launch) {
+    // the driver refused the co-scheduled launch (attribute combination or
+    // too large a grid): launch without it only if every CTA fits at once
+    (void)cudaGetLastError();
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNumThreads, plan.total) != cudaSuccess) {
+      (void)cudaGetLastError();
+      per_sm = 0;
+    }
+    SALR_CHECK_ARG((int64_t)per_sm * sm_count() >= ctas, SALR_ERR_CUDA,
+                   "grid of %d CTAs cannot be co-resident (%d per SM): %s", ctas, per_sm, cudaGetErrorString(le));
+    cfg.numAttrs -= 1;
+    coop_launch = 0;
+    le = cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p);
+  }
+  SALR_CUDA_TRY(le);
   const int info[12] = {ctas, p.stages, BM, NG, p.u_mode, p.coop, p.cluster, pdl ? 1 : 0,
-                        cluster_req, cluster_max, (int)plan.total, 0};
+                        cluster_req, cluster_max, (int)plan.total, coop_launch};
   for (int i = 0; i < 12; ++i) g_last_launch[i] = info[i];
   return SALR_OK;
 }

@@ -163,7 +163,7 @@ def _last_launch():
     info = (ctypes.c_int32 * 12)()
     assert _lib.load().salr_debug_last_launch(ctypes.addressof(info)) == 0
     keys = ("ctas", "stages", "bm", "groups", "u_mode", "coop", "cluster", "pdl", "cluster_req", "cluster_max",
-            "smem")
+            "smem", "cooperative")
     return dict(zip(keys, list(info)))
 
 
@@ -191,6 +191,9 @@ def test_split_k_reduction_modes(S, M, adapters):
         y = S.salr_linear(x, s, fused, num_ctas=ctas)
         info = _last_launch()
         seen.add(info["cluster"])
+        if (info["u_mode"] == 1 or info["coop"]) and not info["pdl"]:
+            # CTAs wait on each other: the launch must be co-scheduled
+            assert info["cooperative"] == 1, info
         assert_close(y.cpu().numpy(), ref, f"M={M} ctas={ctas} {info}")
         y2 = S.salr_linear(x, s, fused, num_ctas=ctas)
         assert torch.equal(y, y2)  # run-to-run determinism of every mode

@@ -19,7 +19,9 @@ ap.add_argument("--tokens", type=int, default=32)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--no-adapters", action="store_true")
 a = ap.parse_args()
-K, N = synthetic.LLAMA3_8B_LINEARS[a.shape]
+# the bench stack's fused launches too: q|k|v and gate|up share their input
+SHAPES = dict(synthetic.LLAMA3_8B_LINEARS, qkv=(4096, 6144), gateup=(4096, 28672))
+K, N = SHAPES[a.shape]
 g = torch.Generator(device="cuda").manual_seed(0)
 w = (torch.randn(K, N, generator=g, device="cuda") * 0.02).bfloat16()
 w = torch.where(w.float().abs() < 0.02 * 0.6744897501960817, torch.zeros_like(w), w)

@@ -20,7 +20,8 @@ import sys
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(REPO, "gpurun_out")
 PROF = os.path.join(REPO, "profiles")
-TILES_GATE = 112 * 64  # 64x128 tiles of the 4096x14336 gate linear
+TILES = {"gate": 112 * 64, "gateup": 224 * 64}  # 64x128 tiles of 4096x14336 / 4096x28672
+ALG = {"gate": 65950928, "gateup": 131910168}  # K*ceil(N/8) + 2*nnz at p=0.5 (seeded bench matrices)
 
 
 def last_json_line(path):
@@ -84,7 +85,17 @@ def main(tag):
               open(os.path.join(PROF, f"{tag}_launch_list.json"), "w"), indent=1)
 
     summ = {}
-    for name, tokens in (("prof_gate32", 32), ("prof_gate1", 1)):
+    logs = {"prof_gateup32": "ncu_fullgu.log", "prof_gate32": "ncu_full.log", "prof_gate1": "ncu_full1.log",
+            "prof_prefill_gate2048": "ncu_fullpf.log"}
+    for name, shape, tokens in (("prof_gateup32", "gateup", 32), ("prof_gate32", "gate", 32),
+                                ("prof_gate1", "gate", 1), ("prof_prefill_gate2048", "gate", 2048)):
+        alg = ALG[shape]
+        try:  # the profiled script prints the matrix's algorithmic bytes
+            for line in open(os.path.join(OUT, logs[name])):
+                if line.startswith("compressed_bytes"):
+                    alg = int(line.split()[1])
+        except OSError:
+            pass
         rep = os.path.join(OUT, name + ".ncu-rep")
         if not os.path.exists(rep):
             continue
@@ -95,15 +106,18 @@ def main(tag):
         rd = f(m["dram__bytes_read.sum"]) * scale[units["dram__bytes_read.sum"]]
         wr = f(m["dram__bytes_write.sum"]) * scale[units["dram__bytes_write.sum"]]
         summ[name] = {
-            "kernel": "salr_linear_kernel (gate 4096x14336, p=0.5, r16+r16 adapters, TB2 compute format)",
+            "kernel": m["Kernel Name"][:60],
+            "shape": shape,
             "tokens": tokens,
             "duration_us_under_ncu": dur,
             "dram_read_bytes": rd,
             "dram_write_bytes": wr,
             "traffic_bytes_per_launch": rd + wr,
-            "algorithmic_compressed_bytes": 65950928,
-            "smem_lsu_wavefronts_per_tile": f(m["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]) / TILES_GATE,
-            "warp_instructions_per_tile": f(m["smsp__inst_executed.sum"]) / TILES_GATE,
+            "algorithmic_compressed_bytes": alg,
+            "smem_lsu_wavefronts_per_tile": f(m["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]) / TILES[shape],
+            "warp_instructions_per_tile": f(m["smsp__inst_executed.sum"]) / TILES[shape],
+            "dram_throughput_pct": f(m.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "nan")),
+            "issue_active_pct": f(m.get("smsp__issue_active.avg.pct_of_peak_sustained_active", "nan")),
             "ipc_active": f(m["sm__inst_executed.avg.per_cycle_active"]),
             "tensor_pipe_pct_elapsed": f(m["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]),
             "note": "ncu --set full --clock-control none, cold cache, serialized",
@@ -111,8 +125,12 @@ def main(tag):
         with open(os.path.join(PROF, f"{tag}_ncu_{name}_details.csv"), "w") as fo:
             fo.write(subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
                                     text=True).stdout)
-    if "prof_gate32" in summ:
-        summ["traffic_bytes_per_launch"] = summ["prof_gate32"]["traffic_bytes_per_launch"]
+    if "prof_gateup32" in summ:  # the bench's dominant launch (bench.py reads these three keys)
+        summ["launch"] = "gateup M=32"
+        summ["traffic_bytes_per_launch"] = summ["prof_gateup32"]["traffic_bytes_per_launch"]
+        summ["source"] = (f"profiles/{tag}_ncu_prof_gateup32_details.csv: ncu --set full --clock-control none of "
+                          "one salr_linear_kernel launch of the bench's gate|up linear (4096x28672, M=32), "
+                          "dram__bytes_read.sum + dram__bytes_write.sum")
     json.dump(summ, open(os.path.join(PROF, "ncu_summary.json"), "w"), indent=1)
     print(json.dumps({k: v for k, v in summ.items() if k != "traffic_bytes_per_launch"}, indent=1))
 
