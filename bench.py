@@ -407,45 +407,20 @@ def layer_check(lin, x, layer0):
     return worst
 
 
-class StackRunner:
-    """One decode step through the (sharded) stack; all device work on one stream."""
+PLAN = [("qkv", None), ("o", (0, 4096)), ("gateup", None), ("down", (0, 14336))]
 
-    def __init__(self, stack, tokens, world, out_dtype, group=None):
-        import torch
-        import paper_2601_16991_b200 as S
-        self.S, self.stack, self.M, self.world, self.group = S, stack, tokens, world, group
-        dev = torch.device("cuda", torch.cuda.current_device())
-        self.x_in = torch.zeros(tokens, 4096, dtype=torch.bfloat16, device=dev)
-        self.bufs = {name: torch.empty(tokens, stack[0][name][2][1], dtype=torch.bfloat16, device=dev)
-                     for name in STACK_ORDER}
-        self.launches_per_step = 0
 
-    def _gather(self, local, width):
-        """All-gather the column shards of one linear into full rows."""
-        if self.world == 1:
-            return local
-        from paper_2601_16991_b200.sharding import gather_columns
-        return gather_columns(local, width, group=self.group)
-
-    def _linear(self, x, lin, name):
-        s, f, _, _ = lin[name]
-        y = self.S.salr_linear(x, s, f, out=self.bufs[name], check_finite=False, pdl=True)
-        # one fused kernel per linear (M <= 256: U = X @ A_cat is computed in-kernel)
-        self._launches += 1 if self.M <= 256 else 2
-        return self._gather(y, sum(w for _, w in FUSED[name][1]))
-
-    def step(self, x):
-        self._launches = 0
-        h = x
-        for lin in self.stack:
-            qkv = self._linear(h, lin, "qkv")
-            # the stack is linears only (attention is outside the hot path):
-            # o consumes the q columns, down the gate columns
-            o = self._linear(qkv[:, :4096], lin, "o")
-            gu = self._linear(o, lin, "gateup")
-            h = self._linear(gu[:, :14336], lin, "down")
-        self.launches_per_step = self._launches
-        return h
+def make_runner(stack, tokens, world, rank, group=None):
+    """The package's column-sharded stack over this rank's shards: o consumes
+    the q columns of q|k|v and down the gate columns of gate|up (the stack is
+    linears only; attention and the MLP nonlinearity are outside the path),
+    and only those columns are gathered."""
+    from paper_2601_16991_b200.sharding import ShardedLinear, ShardedStack
+    layers = []
+    for lin in stack:
+        layers.append({name: ShardedLinear(s, f, sum(w for _, w in FUSED[name][1]), world, rank)
+                       for name, (s, f, _, _) in lin.items()})
+    return ShardedStack(layers, PLAN, world, rank, group, tokens)
 
 
 def time_steps(fn, steps, warmup, world, sampler_dev):
@@ -558,18 +533,21 @@ def run_salr(args):
     M = args.tokens
 
     # ---- device-timed steps (graph-captured stack)
-    runner = StackRunner(stack, M, world, torch.bfloat16)
+    runner = make_runner(stack, M, world, rank)
     x0 = gen_x(M, dev)
     runner.x_in.copy_(x0)
-    use_graph = world == 1
-    if use_graph:
-        runner.step(runner.x_in)  # compile-free warm call; allocates workspaces
-        torch.cuda.synchronize()
+    use_graph = True
+    runner.step(runner.x_in)  # warm call; allocates workspaces
+    torch.cuda.synchronize()
+    try:  # one CUDA graph per step (NCCL all-gathers are captured too at N > 1)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             out_static = runner.step(runner.x_in)
         step_fn = graph.replay
-    else:
+    except Exception as e:  # pragma: no cover - capture unsupported by this NCCL build
+        print(f"warning: step graph capture failed ({e}); timing eager steps", file=sys.stderr)
+        use_graph = False
+        torch.cuda.synchronize()
         step_fn = lambda: runner.step(runner.x_in)  # noqa: E731
     ms, clocks = time_steps(step_fn, args.steps, args.warmup, world, local)
     ms_per_step = ms / args.steps
@@ -651,7 +629,7 @@ def run_salr(args):
                     per_m[str(mb)] = {"tokens_per_s": tokens_per_s, "ms_per_step": ms_per_step, "clocks": clocks,
                                       "compressed_gbs": comp_bytes / (ms_per_step / 1e3) / 1e9}
                     continue
-                r2 = StackRunner(stack, mb, 1, torch.bfloat16)
+                r2 = make_runner(stack, mb, 1, 0)
                 r2.x_in.copy_(torch.randn(mb, 4096, device=dev).bfloat16())
                 r2.step(r2.x_in)
                 torch.cuda.synchronize()
@@ -678,7 +656,8 @@ def run_salr(args):
             "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic random-init weights/inputs",
-            "config": stack_config(args, world, "CUDA graph per step" if use_graph else "eager (NCCL all-gathers)"),
+            "config": stack_config(args, world, ("CUDA graph per step" + (" (NCCL all-gathers captured)" if world > 1 else ""))
+                                  if use_graph else "eager (NCCL all-gathers)"),
             "compressed_gbs": comp_bytes / (ms_per_step / 1e3) / 1e9,
             "compressed_bytes_per_step": comp_bytes,
             "roofline": roof,

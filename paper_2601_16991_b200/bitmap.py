@@ -279,6 +279,62 @@ class BitmapSparseMatrix:
                 self.records = self.tile_off = None  # TB2 is the one resident format
         return self._tb2
 
+    @classmethod
+    def from_compute_format(cls, rows: int, cols: int, records2: torch.Tensor, tile_off2: torch.Tensor):
+        """A bf16 matrix held only in the TB2 compute format (records built
+        elsewhere: another rank, a file, ``column_shard``).  No kernel runs:
+        the tile headers give nnz and the offsets the largest record."""
+        if records2.dtype != torch.uint8 or records2.dim() != 1 or tile_off2.dim() != 1:
+            raise FormatError("records2 must be a 1-D uint8 tensor and tile_off2 1-D")
+        obj = cls.__new__(cls)
+        obj._init_geometry(rows, cols, "bf16")
+        if int(tile_off2.numel()) != obj.n_tiles + 1:
+            raise ShapeError(f"tile_off2 has {int(tile_off2.numel())} entries, expected {obj.n_tiles + 1}")
+        off = tile_off2.to(torch.int64) & 0xFFFFFFFF
+        if int(off[0]) != 0 or 16 * int(off[-1]) > int(records2.numel()) or bool((off[1:] < off[:-1]).any()):
+            raise CorruptionError("tile_off2 is not a monotone offset table within records2")
+        obj.records = obj.tile_off = None
+        obj._max_rec = None
+        mx = int(16 * (off[1:] - off[:-1]).max()) if off.numel() > 1 else 0
+        obj._tb2 = (records2, tile_off2.to(torch.int32), mx)
+        obj.nnz = _tile_nnz_sum(records2, off[:-1])
+        return obj
+
+    def column_shard(self, c0: int, c1: int) -> "BitmapSparseMatrix":
+        """Columns [c0, c1) as a matrix of their own (multi-GPU column
+        sharding): tiles are stored n-tile-major, so a stripe
+        of whole 128-column tiles is one contiguous run of records -- the
+        shard is a byte-exact copy of that run plus rebased offsets, in every
+        resident format.  c0 must be a multiple of 128 and c1 too unless it
+        is ``cols``."""
+        tn = _lib.TILE_N
+        if not (0 <= c0 < c1 <= self.cols) or c0 % tn or (c1 % tn and c1 != self.cols):
+            raise ShapeError(f"column range [{c0}, {c1}) of {self.cols} is not a whole-tile stripe")
+        t0 = (c0 // tn) * self.n_kt
+        t1 = ((c1 + tn - 1) // tn) * self.n_kt
+
+        def cut(records, tile_off):
+            off = tile_off.to(torch.int64) & 0xFFFFFFFF
+            o0, o1 = int(off[t0]), int(off[t1])
+            return records[16 * o0:16 * o1].clone(), (off[t0:t1 + 1] - o0).to(torch.int32)
+
+        obj = self.__class__.__new__(self.__class__)
+        obj._init_geometry(self.rows, c1 - c0, self.value_dtype)
+        obj.records = obj.tile_off = None
+        if self.records is not None:
+            obj.records, obj.tile_off = cut(self.records, self.tile_off)
+        if self._tb2 is not None:
+            r2, o2 = cut(self._tb2[0], self._tb2[1])
+            oo = o2.to(torch.int64)
+            obj._tb2 = (r2, o2, int(16 * (oo[1:] - oo[:-1]).max()) if oo.numel() > 1 else 0)
+        obj._max_rec = None
+        if obj.records is not None:
+            obj.max_record_bytes  # computed eagerly (never inside a graph capture)
+            obj.nnz = _tile_nnz_sum(obj.records, obj.tile_off.to(torch.int64)[:-1])
+        else:
+            obj.nnz = _tile_nnz_sum(obj._tb2[0], obj._tb2[1].to(torch.int64)[:-1])
+        return obj
+
     def to_bf16(self) -> "BitmapSparseMatrix":
         """The same matrix with bf16 values (the linear kernel's operand
         format); a new object (not cached) for a float32 matrix."""
@@ -294,6 +350,17 @@ class BitmapSparseMatrix:
     def __repr__(self):
         return (f"BitmapSparseMatrix(rows={self.rows}, cols={self.cols}, nnz={self.nnz}, "
                 f"value_dtype={self.value_dtype!r}, device={self.device})")
+
+
+def _tile_nnz_sum(records: torch.Tensor, starts16: torch.Tensor) -> int:
+    """Sum of the per-tile nnz words (u32 header word 3 of every TB / TB2
+    record starting at 16 * starts16) -- plain tensor indexing, any device."""
+    if starts16.numel() == 0:
+        return 0
+    base = 16 * (starts16.to(records.device) & 0xFFFFFFFF) + 12
+    idx = base.unsqueeze(1) + torch.arange(4, device=records.device)
+    b = records[idx].to(torch.int64)
+    return int((b[:, 0] | (b[:, 1] << 8) | (b[:, 2] << 16) | (b[:, 3] << 24)).sum())
 
 
 def encode(m, value_dtype: str = "f32") -> BitmapSparseMatrix:
