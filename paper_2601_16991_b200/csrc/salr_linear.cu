@@ -956,6 +956,55 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
           store_y((size_t)(mc * BM + m) * p.ldy + nt * kTileN + cl, nt * kTileN + cl, acc);
         }
+      } else if (c_last - c_first <= 1) {
+        // two partials (large shapes: tiles split over 2 CTAs), many chunks
+        // per thread: 4-column chunks, kIPT per thread per pass, every
+        // partial of the pass loaded before any sum (one L2 round trip per
+        // pass instead of one per chunk), summed in CTA order
+        constexpr int kIPT = 4;
+        const int items = (r1 - r0) * (kTileN / 4);
+        for (int e0 = etid - t0; e0 < items; e0 += nthr * kIPT) {
+          float4 acc[kIPT];
+          size_t offs[kIPT];
+#pragma unroll
+          for (int i = 0; i < kIPT; ++i) {
+            const int e = e0 + i * nthr;
+            const int m = r0 + e / (kTileN / 4), c4 = 4 * (e % (kTileN / 4));
+            offs[i] = (size_t)m * kTileN + c4;
+            if (e < items) acc[i] = __ldcg(reinterpret_cast<const float4*>(p_first + offs[i]));
+          }
+          for (int c = c_first + 1; c <= c_last; c += 2) {
+            float4 v[2][kIPT];
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int i = 0; i < kIPT; ++i)
+                if (c + j <= c_last && e0 + i * nthr < items)
+                  v[j][i] = __ldcg(reinterpret_cast<const float4*>(p.partials + (size_t)(c + j) * 2 * tile_elems +
+                                                                   offs[i]));
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int i = 0; i < kIPT; ++i)
+                if (c + j <= c_last && e0 + i * nthr < items) {
+                  acc[i].x += v[j][i].x;
+                  acc[i].y += v[j][i].y;
+                  acc[i].z += v[j][i].z;
+                  acc[i].w += v[j][i].w;
+                }
+          }
+#pragma unroll
+          for (int i = 0; i < kIPT; ++i) {
+            const int e = e0 + i * nthr;
+            if (e >= items) continue;
+            const int m = r0 + e / (kTileN / 4), c4 = 4 * (e % (kTileN / 4));
+            const size_t o = (size_t)(mc * BM + m) * p.ldy + nt * kTileN + c4;
+            store_y(o, nt * kTileN + c4, acc[i].x);
+            store_y(o + 1, nt * kTileN + c4 + 1, acc[i].y);
+            store_y(o + 2, nt * kTileN + c4 + 2, acc[i].z);
+            store_y(o + 3, nt * kTileN + c4 + 3, acc[i].w);
+          }
+        }
       } else {
         // one 4-column chunk per thread and pass; the partials of a chunk are
         // loaded in batches of 8 independent 16-byte loads

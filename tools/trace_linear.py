@@ -26,7 +26,7 @@ ap.add_argument("--launches", type=int, default=4)
 ap.add_argument("--detail", type=int, default=4, help="print the event sequence of the N latest CTAs")
 ap.add_argument("--graph", action="store_true", help="capture the launches (PDL-chained) in one CUDA graph")
 a = ap.parse_args()
-K, N = synthetic.LLAMA3_8B_LINEARS[a.shape]
+K, N = dict(synthetic.LLAMA3_8B_LINEARS, qkv=(4096, 6144), gateup=(4096, 28672))[a.shape]
 g = torch.Generator(device="cuda").manual_seed(0)
 w = (torch.randn(K, N, generator=g, device="cuda") * 0.02).bfloat16()
 w = torch.where(w.float().abs() < 0.02 * 0.6744897501960817, torch.zeros_like(w), w)
