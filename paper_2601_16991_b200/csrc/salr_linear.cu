@@ -91,10 +91,13 @@ constexpr int kCtrlEpoch = 0, kCtrlDone = 1, kCtrlReady = 2, kCtrlUsed = 4, kCtr
 constexpr int kUSlice = 64;  // K rows per dynamically claimed U slice
 constexpr int kDoneTicketOff = 16 * 1024;  // second counter per split tile (workspace ticket area)
 constexpr int kUAccElems = 256 * 128;  // per parity buffer: M <= 256 rows x r_pad <= 128
-constexpr int kNumDecWarps = 16;
-constexpr int kNumThreads = 800;               // 25 warps
+// Warp layout for NG decoder groups of four warps (one per TMEM lane quarter):
+// warps 0-3 producers / MMA / publisher, 4 .. 4+4NG-1 decoders, then four
+// epilogue warps.
 constexpr int kFirstDecWarp = 4;
-constexpr int kFirstEpiWarp = 20;
+__host__ __device__ constexpr int num_dec_warps(int ng) { return 4 * ng; }
+__host__ __device__ constexpr int first_epi_warp(int ng) { return kFirstDecWarp + 4 * ng; }
+__host__ __device__ constexpr int num_threads(int ng) { return 32 * (first_epi_warp(ng) + 4); }
 constexpr uint32_t kAdTileBytes = 128 * 128;   // B_cat^T tile: 128 rows x 64 bf16
 constexpr size_t kSmemMax = 232448;            // 227 KB opt-in per block
 constexpr size_t kSmemMaxLinear = kSmemMax - 128;  // minus the decoders' static nibble table
@@ -197,18 +200,27 @@ __device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t 
 // each serial role is split across warps that work on different units
 // concurrently: two producers (even / odd units), two row-base warps, and
 // kDecGroups decoder groups (group g decodes units it = g mod kDecGroups).
-constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPub = 2;  // warp 3 idle
-constexpr int kWarpProd1 = 24;
+// Roles spread over the four SM sub-partitions (warp w issues on SMSP w % 4,
+// which also hosts four decoder warps and one epilogue warp): the two
+// producers on SMSPs 0 and 3, the MMA issuer on 1, the publisher on 2.  The
+// producers and the MMA warp are the per-unit serial path of the CTA, so no
+// two of them share a sub-partition.
+constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPub = 2;
+constexpr int kWarpProd1 = 3;
 
 template <int BM, int kDecGroups>
-__global__ void __launch_bounds__(kNumThreads, 1)
+__global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     salr_linear_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
                        const __grid_constant__ CUtensorMap uhimap, const __grid_constant__ CUtensorMap ulomap,
                        const LinearParams p) {
   constexpr int NACC = nacc_for(BM);
   constexpr int ACOLS = acc_cols_for(BM);
   constexpr uint32_t IDESC = idesc_bf16_f32(128, BM);
-  constexpr int WPG = kNumDecWarps / kDecGroups;  // decoder warps per group
+  constexpr int kNumDecWarps = num_dec_warps(kDecGroups);
+  constexpr int kFirstEpiWarp = first_epi_warp(kDecGroups);
+  constexpr int kNumThreads = num_threads(kDecGroups);
+  constexpr int kUWide = 32 * (kNumDecWarps + 4);  // decoder + epilogue threads (wide U path)
+  constexpr int WPG = 4;                          // decoder warps per group: one per lane quarter
   constexpr int RPW = 4 * kTileK / WPG;           // rows per decoder warp (all 4 lane quarters per group)
 
   extern __shared__ uint8_t smem_raw[];
@@ -256,20 +268,16 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   const bool early_split = !p.cluster && (u_begin % p.n_kt != 0 || first_seg_end0 - u_begin < p.n_kt) &&
                            first_seg_end0 < u_end;
 
-  // ---- producer state (warps kWarpProd0 / kWarpProd1, units of one parity).
+  // ---- producers.  kWarpProd0 streams the weight records of every unit,
+  // kWarpProd1 the X tiles: each loop is the minimum per unit (wait for the
+  // stage to drain, one elected copy), since the producers sit on the CTA's
+  // serial path and share their SM sub-partitions with busy decoder warps.
   // Record offsets are fetched 32 units at a time, one chunk ahead, one
   // coalesced load per lane, so the issue loop never waits on a global load.
-  // Each multi-instance role owns the stages s = instance (mod instances), so
-  // an instance never waits on a stage two phases ahead (mbarrier parity
-  // waits cannot tell those apart): the host picks S as a multiple of the
-  // decoder group count, and the producers / row-base warps run as pairs only
-  // when S is even.
-  const int NP = (S % 2 == 0) ? 2 : 1;
-  const int pk = warp == kWarpProd1 ? 1 : 0;
   uint32_t co0 = 0, co1 = 0, no0 = 0, no1 = 0;
   int chunk = u_begin;
-  int pv = u_begin + pk;  // next unit to issue (this producer's parity)
-  int ps = pk;            // < S whenever this producer is active
+  int pv = u_begin;  // next unit to issue
+  int ps = 0;        // its stage
   uint32_t pph = 0;
   const uint64_t pol_stream = l2_policy_evict_first();
   auto load_chunk = [&](int c0, uint32_t& o0, uint32_t& o1) {
@@ -281,21 +289,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       o1 = __ldg(p.tile_off + t + 1);
     }
   };
-  // X tile of unit v into stage st (the input; may have to wait for the
-  // preceding kernel under programmatic dependent launch)
-  auto issue_x = [&](int v, int st) {
-    const int kt = v % p.n_kt;
-    const int mc = v / tiles_per_mc;
-    tma_2d_g2s(xbuf + (size_t)st * BM * 128, &xmap, kt * kTileK, mc * BM, &xfull[st]);
-    mbar_arrive_expect_tx(&xfull[st], BM * 128);
-  };
-  // Issue unit pv.  The copies go out before arrive.expect_tx (the phase
-  // cannot complete before the arrive, and issuing the copy first keeps it
-  // off the arrive's latency).  The first ring's worth of units never waits
-  // for `empty`.  with_x = false defers the X tile (see the PDL prologue).
-  auto issue_one = [&](bool with_x) {
+  // Record of unit pv into its stage.  The copy goes out before
+  // arrive.expect_tx (the phase cannot complete before the arrive, and
+  // issuing the copy first keeps it off the arrive's latency).  The first
+  // ring's worth of units never waits for `empty`.
+  auto issue_rec = [&]() {
     if (lane == 0) SALR_TRACE_UNIT(8, pv - u_begin);
-    while (pv - chunk >= 32) {
+    if (pv - chunk >= 32) {
       chunk += 32;
       co0 = no0;
       co1 = no1;
@@ -310,19 +310,18 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const uint32_t bytes = (p.dbg & 2) ? 0u : (o1 - o0) * 16u;
       if (bytes) bulk_g2s_hint(recbuf + (size_t)ps * p.rec_slot, p.records + (size_t)o0 * 16u, bytes, &full[ps], pol_stream);
       mbar_arrive_expect_tx(&full[ps], bytes);
-      if (with_x && !(p.dbg & 16)) issue_x(pv, ps);
       SALR_TRACE_UNIT(0, pv - u_begin);
     }
     __syncwarp();
-    ps += NP;
-    if (ps >= S) { ps -= S; pph ^= 1; }
-    pv += NP;
+    if (++ps == S) { ps = 0; pph ^= 1; }
+    ++pv;
   };
 
-  const bool producer = warp == kWarpProd0 || (warp == kWarpProd1 && NP == 2);
   if (warp == kWarpProd0 || warp == kWarpProd1) {
-    load_chunk(u_begin, co0, co1);
-    load_chunk(u_begin + 32, no0, no1);
+    if (warp == kWarpProd0) {
+      load_chunk(u_begin, co0, co1);
+      load_chunk(u_begin + 32, no0, no1);
+    }
     if (warp == kWarpProd0 && lane == 0) {
       prefetch_tmap(&xmap);
       if (p.ra) {
@@ -333,7 +332,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       for (int s = 0; s < S; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&xfull[s], 1);
-        mbar_init(&empty[s], 1);
+        mbar_init(&empty[s], 1);  // the MMA commit: decode and X tile of the stage consumed
         mbar_init(&decoded[s], WPG);
       }
       for (int b = 0; b < 2; ++b) {
@@ -347,12 +346,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     named_bar_sync(2, 64);  // barriers initialised before either producer uses them
     if (threadIdx.x == 0) SALR_TRACE(21);
-    // Start streaming before the CTA-wide setup barrier: this producer's share
-    // of the first ring's worth of units of the first output tile (never blocks).
-    const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
-    const int pre = min(first_seg_end, u_begin + S);
-    if (producer)
-      while (pv < pre) issue_one(false);
+    // Start streaming before the CTA-wide setup barrier: the first ring's
+    // worth of records of the first output tile (never blocks).
+    if (warp == kWarpProd0) {
+      const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
+      const int pre = min(first_seg_end, u_begin + S);
+      while (pv < pre) issue_rec();
+    }
     if (threadIdx.x == 0) SALR_TRACE(23);
   }
   // ---- in-kernel U (u_mode 1) geometry.  K is cut into slices of kUSlice
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (warp >= (wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4 && u_staged_fn()) {
       const int ut = (warp - (wide ? kFirstDecWarp : kFirstEpiWarp)) * 32 + (int)lane;
       const int nsl = (p.K + kUSlice - 1) / kUSlice;
-      if ((int)blockIdx.x < nsl) u_load_a((int)blockIdx.x, ut, wide ? 640 : 128);
+      if ((int)blockIdx.x < nsl) u_load_a((int)blockIdx.x, ut, wide ? kUWide : 128);
       const int pf = G + (int)blockIdx.x;  // a slice another CTA may claim
       if (ut == 0 && pf < nsl)
         prefetch_l2_bulk(p.acat + (size_t)pf * kUSlice * 64 * p.ra,
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // nibble table of the decoders: static shared memory, so its address is a
   // compile-time constant folded into the decoders' loads
   __shared__ __align__(128) uint64_t s_lut[16];
-  if (warp == 3 && lane < 16) s_lut[lane] = nib_lut_entry(lane);
+  if (warp == kWarpPub && lane < 16) s_lut[lane] = nib_lut_entry(lane);
   const uint32_t lut_s = smem_u32(s_lut);
   if (warp == kWarpMma) {
     tmem_alloc(tmem_slot, 512);
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // delay; measured: with 16 units per CTA the decoders are better off
   // starting to decode).
   const bool u_wide = u_geom_wide();
-  const int kUThreads = u_wide ? 640 : 128;
+  const int kUThreads = u_wide ? kUWide : 128;
   if (p.u_mode == 1 && warp >= (u_wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4) {
     const int ut = (warp - (u_wide ? kFirstDecWarp : kFirstEpiWarp)) * 32 + (int)lane;
     const int rp = 64 * p.ra;
@@ -543,25 +543,43 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (ut == 0 && done) SALR_TRACE(13);
   }
 
-  if (warp == kWarpProd0 || warp == kWarpProd1) {
-    // ================= TMA producers.  Weights never depend on the preceding
-    // kernel; the input X may (it can be that kernel's output): wait for it
-    // only now -- after the CTA-wide setup, so the decoders already work on
-    // the first ring -- then send the X tiles of the units already in flight.
+  if (warp == kWarpProd0) {
+    // ================= record producer: weights never depend on the
+    // preceding kernel, so it streams on without waiting for it
+    if (lane == 0) SALR_TRACE(1);
+    while (pv < u_end) issue_rec();
+    if (lane == 0) SALR_TRACE(2);
+  } else if (warp == kWarpProd1) {
+    // ================= X producer: the input may be the preceding kernel's
+    // output -- wait for it only now, after the CTA-wide setup, so the
+    // decoders already work on the first ring.  (k-tile, m-chunk) advance
+    // without divisions.  Both producers wait for the same `empty` phase (the
+    // MMA commit of the stage's previous unit), so an X tile never lands in
+    // a stage whose previous X tile an MMA may still read.
     pdl_wait();
-    if (threadIdx.x == 0) SALR_TRACE(24);
-    if (lane == 0 && producer) {
-      const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
-      const int pre = min(first_seg_end, u_begin + S);
-      if (!(p.dbg & 16))
-        for (int v = u_begin + pk; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
+    if (threadIdx.x == 32 * kWarpProd1) SALR_TRACE(24);
+    int kt = u_begin % p.n_kt, mc = u_begin / tiles_per_mc, rem = tiles_per_mc - u_begin % tiles_per_mc;
+    int xs = 0;
+    uint32_t xph = 0;
+    for (int v = u_begin; v < u_end; ++v) {
+      if (v - u_begin >= S) mbar_wait(&empty[xs], xph ^ 1);
+      if (lane == 0) {
+        if (!(p.dbg & 16)) {
+          tma_2d_g2s(xbuf + (size_t)xs * BM * 128, &xmap, kt * kTileK, mc * BM, &xfull[xs]);
+          mbar_arrive_expect_tx(&xfull[xs], BM * 128);
+        } else {
+          mbar_arrive(&xfull[xs]);
+        }
+      }
+      __syncwarp();
+      if (++xs == S) { xs = 0; xph ^= 1; }
+      if (++kt == p.n_kt) kt = 0;
+      if (--rem == 0) {
+        rem = tiles_per_mc;
+        ++mc;
+      }
     }
-    __syncwarp();
-    if (threadIdx.x == 0) SALR_TRACE(28);
-    if (lane == 0 && pk == 0) SALR_TRACE(1);
-    if (producer)
-      while (pv < u_end) issue_one(true);
-    if (lane == 0 && pk == 0) SALR_TRACE(2);
+    if (threadIdx.x == 32 * kWarpProd1) SALR_TRACE(28);
   } else if (warp == kWarpPub) {
     // ================= publisher: releases the first split partial at GPU
     // scope (fence + ticket) so the epilogue warps never stall on it
@@ -643,8 +661,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 #define SALR_MMA_UNIT(K)                                                                              \
   case K:                                                                                             \
     if (v >= seg_end) break;                                                                          \
-    mbar_wait_addr(dec0 + 8u * (K), ph);                                                              \
-    mbar_wait_addr(xf0 + 8u * (K), ph);                                                               \
+    SALR_TRACE_UNIT(2, v - u_begin);                                                                  \
+    mbar_wait2_addr(dec0 + 8u * (K), xf0 + 8u * (K), ph);                                            \
     tc_fence_after();                                                                                 \
     SALR_TRACE_UNIT(6, v - u_begin);                                                                  \
     mma_ktile_ts_imm<kTm + a_col0 + 32u * (K)>(acc, lo0 + (K) * kLoStep, bhi, IDESC, v != u ? 1u : 0u, \
@@ -1053,9 +1071,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const int mc = u / (p.n_kt * p.n_nt);
       const int b = NACC == 2 ? (seg & 1) : 0;
       const uint32_t acc_ph = (uint32_t)((NACC == 2 ? seg >> 1 : seg) & 1);
-      // long wait: try_wait suspends the warp in hardware (no issue slots)
-      // and wakes it as soon as the phase completes
-      mbar_wait(&acc_full[b], acc_ph);
+      // long wait (a whole output tile's k-loop): backoff polling, see
+      // mbar_wait_backoff -- the decoders keep the issue slots
+      mbar_wait_backoff(&acc_full[b], acc_ph, 256);
       tc_fence_after();
       if (etid == 0 && seg == 0) SALR_TRACE(7);
       // partial slot of this CTA: 0 for its first segment, 1 otherwise
@@ -1401,6 +1419,7 @@ static int pick_bm(int64_t M) {
 // Deepest ring that fits shared memory and TMEM (slots sized for the largest
 // record of the matrix: ~9.6 KB at 50% sparsity instead of the 17.4 KB worst
 // case).
+static int pref_groups();
 static int max_stages(int bm, int ra, uint32_t rec_slot, int cap) {
   const int acc = nacc_for(bm) * acc_cols_for(bm);
   const int tmem_stages = (512 - ((acc + 31) & ~31)) / 32;
@@ -1409,7 +1428,8 @@ static int max_stages(int bm, int ra, uint32_t rec_slot, int cap) {
   int s = cap;
   if (s > tmem_stages) s = tmem_stages;
   while (s > 1 && smem_plan(bm, s, ra, rec_slot).total > kSmemMaxLinear) --s;
-  if (s > 4) s &= ~3;  // a multiple of the decoder group count
+  const int ng = pref_groups();
+  if (s > ng) s -= s % ng;  // a multiple of the decoder group count
   return s;
 }
 
@@ -1433,7 +1453,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctas);
-  cfg.blockDim = dim3(kNumThreads);
+  cfg.blockDim = dim3(num_threads(NG));
   cfg.dynamicSmemBytes = plan.total;
   cfg.stream = s;
   cudaLaunchAttribute attr[3];
@@ -1496,7 +1516,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   int coop_launch = 0;
   if ((p.u_mode == 1 || p.coop) && pdl) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNumThreads, plan.total) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, num_threads(NG), plan.total) != cudaSuccess) {
       (void)cudaGetLastError();
       per_sm = 1;
     }
@@ -1515,7 +1535,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
     // too large a grid): launch without it only if every CTA fits at once
     (void)cudaGetLastError();
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNumThreads, plan.total) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, num_threads(NG), plan.total) != cudaSuccess) {
       (void)cudaGetLastError();
       per_sm = 0;
     }
@@ -1532,17 +1552,21 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   return SALR_OK;
 }
 
-// Decoder groups: 4 by default (SALR_DEC_GROUPS overrides for experiments),
-// reduced to a divisor of the ring depth (stage ownership, see the kernel).
-static int dec_groups(int stages) {
+// Decoder groups of four warps: 4 by default (SALR_DEC_GROUPS overrides in
+// debug builds), reduced to a divisor of the ring depth (stage ownership,
+// see the kernel).
+static int pref_groups() {
   static int g = 0;
   if (!g) {
     const char* e = dbg_env("SALR_DEC_GROUPS");
     g = e ? atoi(e) : 4;
-    if (g != 1 && g != 2 && g != 4) g = 4;
+    if (g < 1 || g > 4) g = 4;
   }
-  int ng = g;
-  while (ng > 1 && stages % ng) ng >>= 1;
+  return g;
+}
+static int dec_groups(int stages) {
+  int ng = pref_groups();
+  while (ng > 1 && stages % ng) --ng;
   return ng;
 }
 
@@ -1551,6 +1575,7 @@ static int launch_linear(const CUtensorMap* maps, const LinearParams& p, int cta
   switch (dec_groups(p.stages)) {
     case 1: return launch_linear_g<BM, 1>(maps, p, ctas, s, pdl);
     case 2: return launch_linear_g<BM, 2>(maps, p, ctas, s, pdl);
+    case 3: return launch_linear_g<BM, 3>(maps, p, ctas, s, pdl);
     default: return launch_linear_g<BM, 4>(maps, p, ctas, s, pdl);
   }
 }

@@ -103,6 +103,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 #endif
 }
+// Long, latency-tolerant waits (an epilogue warp idle for a whole output
+// tile): poll with a plain nanosleep backoff.  A suspended try_wait is woken
+// by every mbarrier update of the CTA (hundreds per microsecond in the decode
+// pipeline), so a warp parked in it for ~20 us re-polls hundreds of times
+// and takes issue slots from the decoders on its SM sub-partition; the
+// backoff bounds that to ~1 poll per max_ns at <= max_ns added latency.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t phase, uint32_t max_ns) {
+  uint32_t ns = 32;
+  while (!mbar_test_wait(bar, phase)) {
+    __nanosleep(ns);
+    ns = ns < max_ns ? 2 * ns : max_ns;
+  }
+}
 // Spinning wait (no suspension) for very short expected waits.
 __device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t phase) {
   while (!mbar_test_wait(bar, phase)) {
@@ -402,6 +415,19 @@ __device__ __forceinline__ void mbar_wait_addr(uint32_t bar, uint32_t phase) {
       "r"(phase), "n"(SALR_WAIT_HINT_NS)
       : "memory");
 #endif
+}
+// Wait for two barriers at once (same parity): both probes are in flight
+// together, so the waiter pays one probe latency, not two.
+__device__ __forceinline__ void mbar_wait2_addr(uint32_t bar0, uint32_t bar1, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1;\n\t"
+      "W_%=:\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p0, [%0], %2;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p1, [%1], %2;\n\t"
+      "and.pred p0, p0, p1;\n\t"
+      "@!p0 bra W_%=;\n\t}" ::"r"(bar0),
+      "r"(bar1), "r"(phase)
+      : "memory");
 }
 __device__ __forceinline__ uint32_t mbar_test_addr(uint32_t bar, uint32_t phase) {
   uint32_t ok;

@@ -50,7 +50,7 @@ dd = b[148 * 32:].view(16, 64).cpu()
 c0 = int(dd[7, 0])
 us = lambda v: (int(v) - c0) / a.mhz  # noqa: E731
 cols = [(8, "iss in"), (9, "iss shfl"), (10, "iss empty"), (0, "issue"), (1, "full"), (3, "dec0"), (4, "dec3"),
-        (6, "mma rdy"), (5, "mma iss")]
+        (2, "mma wait"), (6, "mma rdy"), (5, "mma iss")]
 print("unit " + " ".join(f"{n:>8s}" for _, n in cols))
 rows = []
 for i in range(min(a.units, 64)):
