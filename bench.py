@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--batches", default="1,8,32", help="extra decode batch sizes reported per-M")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--chain", action="store_true",
+                    help="one persistent launch per layer (salr_chain) instead of one launch per linear")
     return ap.parse_args()
 
 
@@ -410,7 +412,7 @@ def layer_check(lin, x, layer0):
 PLAN = [("qkv", None), ("o", (0, 4096)), ("gateup", None), ("down", (0, 14336))]
 
 
-def make_runner(stack, tokens, world, rank, group=None):
+def make_runner(stack, tokens, world, rank, group=None, chain=None):
     """The package's column-sharded stack over this rank's shards: o consumes
     the q columns of q|k|v and down the gate columns of gate|up (the stack is
     linears only; attention and the MLP nonlinearity are outside the path),
@@ -420,7 +422,7 @@ def make_runner(stack, tokens, world, rank, group=None):
     for lin in stack:
         layers.append({name: ShardedLinear(s, f, sum(w for _, w in FUSED[name][1]), world, rank)
                        for name, (s, f, _, _) in lin.items()})
-    return ShardedStack(layers, PLAN, world, rank, group, tokens)
+    return ShardedStack(layers, PLAN, world, rank, group, tokens, chain=chain)
 
 
 def time_steps(fn, steps, warmup, world, sampler_dev):
@@ -533,7 +535,7 @@ def run_salr(args):
     M = args.tokens
 
     # ---- device-timed steps (graph-captured stack)
-    runner = make_runner(stack, M, world, rank)
+    runner = make_runner(stack, M, world, rank, chain=args.chain)
     x0 = gen_x(M, dev)
     runner.x_in.copy_(x0)
     use_graph = True
@@ -629,7 +631,7 @@ def run_salr(args):
                     per_m[str(mb)] = {"tokens_per_s": tokens_per_s, "ms_per_step": ms_per_step, "clocks": clocks,
                                       "compressed_gbs": comp_bytes / (ms_per_step / 1e3) / 1e9}
                     continue
-                r2 = make_runner(stack, mb, 1, 0)
+                r2 = make_runner(stack, mb, 1, 0, chain=args.chain)
                 r2.x_in.copy_(torch.randn(mb, 4096, device=dev).bfloat16())
                 r2.step(r2.x_in)
                 torch.cuda.synchronize()

@@ -192,6 +192,32 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
                         int64_t r_pad, void* y, int y_dtype, int64_t ldy, void* workspace,
                         size_t workspace_bytes, int stages, int num_ctas, int flags, void* stream);
 
+/* ---- chained linears (one persistent launch; no reference counterpart:
+ * the reference runs pipelined_forward once per linear, pipeline.py:275-331,
+ * and this is L such calls fused for a decode step's linear chain).
+ * Linear l computes y_l = x_l @ W_l [+ (x_l @ A_cat_l) @ B_cat_l] in bf16 out,
+ * where x_0 = x0 (M x K_0, ld ldx0) and x_l = columns [0, K_l) of y_{l-1}
+ * (ld ldy_{l-1}; K_l <= N_{l-1}).  Records are TB2 (salr_tb2_*), adapters
+ * as in salr_linear_forward (r_pad 0 / 64 / 128).  1 <= L <= 4, M <= 256.
+ * Results equal L salr_linear_forward calls with the same grid (the SM
+ * count).  The workspace's first salr_chain_workspace_zero_bytes() bytes
+ * must be zero once, at allocation (counters reset themselves). */
+typedef struct {
+  const uint8_t* records;
+  const uint32_t* tile_off;
+  int64_t max_record_bytes;
+  int64_t K, N;
+  const void* acat;
+  const void* bcat_t;
+  int64_t r_pad;
+  void* y;
+  int64_t ldy;
+} salr_chain_linear_t;
+size_t salr_chain_workspace_bytes(int64_t M, int L);
+size_t salr_chain_workspace_zero_bytes(void);
+int salr_chain_forward(const salr_chain_linear_t* lin, int L, const void* x0, int64_t M, int64_t ldx0,
+                       void* workspace, size_t workspace_bytes, int flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

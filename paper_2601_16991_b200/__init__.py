@@ -20,7 +20,8 @@ from .bitmap import (BitmapSparseMatrix, build_lut, bytes_per_row, compression_r
                      decode, decode_block, encode, header_bytes, kept_count, popcount8, read_container,
                      write_container)
 from .pipeline import (BenchResult, PipelineConfig, PipelineProbe, SlotState, bench, launch_count,
-                       pipelined_forward, pipelined_matmul, reset_launch_count, salr_linear, validate_transitions)
+                       pipelined_forward, pipelined_matmul, reset_launch_count, salr_chain, salr_linear,
+                       validate_transitions)
 from .prune import PruneConfig, PruneMethod, build_mask, prune
 
 __version__ = "0.1.0"

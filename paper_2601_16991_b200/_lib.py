@@ -54,7 +54,16 @@ _SIGS = {
     "salr_debug_last_launch": ([_vp], _int),
     "salr_linear_forward": ([_vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _int, _i64,
                              _vp, ctypes.c_size_t, _int, _int, _int, _vp], _int),
+    "salr_chain_workspace_bytes": ([_i64, _int], ctypes.c_size_t),
+    "salr_chain_workspace_zero_bytes": ([], ctypes.c_size_t),
+    "salr_chain_forward": ([_vp, _int, _vp, _i64, _i64, _vp, ctypes.c_size_t, _int, _vp], _int),
 }
+
+
+class ChainLinear(ctypes.Structure):
+    """salr_chain_linear_t (include/salr_b200.h)."""
+    _fields_ = [("records", _vp), ("tile_off", _vp), ("max_record_bytes", _i64), ("K", _i64), ("N", _i64),
+                ("acat", _vp), ("bcat_t", _vp), ("r_pad", _i64), ("y", _vp), ("ldy", _i64)]
 EXPORTS = tuple(_SIGS)
 
 _lock = threading.Lock()

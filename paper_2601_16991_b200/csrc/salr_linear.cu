@@ -39,6 +39,7 @@
 //   * M > 256: salr_prefill.cuh (one decode per weight tile per 512 tokens).
 
 #include <algorithm>
+#include <cstring>
 #include <cstdint>
 #include <cstdlib>
 #include <cuda.h>
@@ -199,6 +200,76 @@ __device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t 
 // SM cycles of latency on B200 (measured, tools/ubench/ubench_sync.cu), so
 // each serial role is split across warps that work on different units
 // concurrently: two producers (even / odd units), two row-base warps, and
+// TB2 tile decoder, one warp: TMEM lane quarter q (output columns 32q..32q+31),
+// all 64 rows.  Per lane (one output column) and 4-row band the values are
+// contiguous: the band's run starts at bandoff[q][b] + (exclusive warp prefix
+// of the band counts), and four zero-extended loads plus two byte permutes
+// driven by the nibble table expand the 4 rows -- no per-element rank
+// popcounts.  Writes the lane's 32 bf16-pair columns of the A operand with
+// tcgen05.st (the caller waits and fences).
+__device__ __forceinline__ void decode_tile_tb2(uint32_t rec_s, uint32_t taddr, int q, uint32_t lane,
+                                                uint32_t lut_s) {
+  const uint2 mw = lds_v2_u32(rec_s + kT2Mask + 8u * (32u * q + lane));
+  // 4-bit band counts as bytes: c[0] bands 0,2,4,6; c[1] 1,3,5,7;
+  // c[2] 8,10,12,14; c[3] 9,11,13,15
+  uint32_t nl = mw.x - ((mw.x >> 1) & 0x55555555u);
+  uint32_t nh = mw.y - ((mw.y >> 1) & 0x55555555u);
+  nl = (nl & 0x33333333u) + ((nl >> 2) & 0x33333333u);
+  nh = (nh & 0x33333333u) + ((nh >> 2) & 0x33333333u);
+  const uint32_t c[4] = {nl & 0x0F0F0F0Fu, (nl >> 4) & 0x0F0F0F0Fu, nh & 0x0F0F0F0Fu, (nh >> 4) & 0x0F0F0F0Fu};
+  uint32_t e[4] = {c[0], c[1], c[2], c[3]};
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {  // inclusive scan, byte lanes (<= 128)
+    uint32_t t[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t[j] = __shfl_up_sync(0xffffffffu, e[j], d);
+    if ((int)lane >= d) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) e[j] += t[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) e[j] -= c[j];
+  const uint32_t goff = q ? lds_u32(rec_s + 4u * (uint32_t)(q - 1)) : 0u;
+  const uint32_t vb = rec_s + kT2Val + 2u * goff;
+  const uint4 bo0 = lds_v4_u32(rec_s + kT2BandOff + 32u * q);
+  const uint4 bo1 = lds_v4_u32(rec_s + kT2BandOff + 32u * q + 16u);
+  const uint32_t bo[8] = {bo0.x, bo0.y, bo0.z, bo0.w, bo1.x, bo1.y, bo1.z, bo1.w};
+#pragma unroll
+  for (int c4 = 0; c4 < 4; ++c4) {  // 4 bands -> 8 TMEM columns
+    uint32_t packed[8];
+#pragma unroll
+    for (int i = 0; i < 4; i += 2) {
+      const int b = 4 * c4 + i;  // bands b, b+1
+      // byte offsets of both bands' runs in 16-bit lanes: (prefix + band
+      // offset) * 2; byte prefixes are < 128, so sign-replicating selector
+      // nibbles give the zero bytes
+      const int j = (b & 7) >> 1;
+      const uint32_t pe = prmt(e[b >= 8 ? 2 : 0], e[b >= 8 ? 3 : 1],
+                               (uint32_t)j | ((0x8u | j) << 4) | ((4u + j) << 8) | ((0x8u | j) << 12));
+      const uint32_t pr2 = pe + pe + (bo[b >> 1] + bo[b >> 1]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int bb = b + h;
+        const uint32_t r = h ? vb + (pr2 >> 16) : vb + (pr2 & 0xFFFFu);
+        const int sh = 4 * (bb & 7);
+        const uint32_t word = bb < 8 ? mw.x : mw.y;
+        // nibble -> table entry (8 bytes): selectors of both row pairs and
+        // the byte offset of pair 1's first value.  Absent elements need no
+        // predicate: the selectors pick zero bytes of the zero-extended loads.
+        const uint32_t nib8 = (sh >= 3 ? (word >> (sh - 3)) : (word << 3)) & 0x78u;
+        const uint2 ent = lds_v2_u32(lut_s | nib8);
+        const uint32_t r2 = r + (ent.x >> 16);
+        const uint32_t a0 = lds_u16z(r), a1 = lds_u16z(r + 2u);
+        const uint32_t b0 = lds_u16z(r2), b1 = lds_u16z(r2 + 2u);
+        packed[2 * (i + h)] = prmt(a0, a1, ent.x);
+        packed[2 * (i + h) + 1] = prmt(b0, b1, ent.y);
+      }
+    }
+    SALR_TMEM_ST_X8(taddr + 8u * c4, packed);
+  }
+}
+
 // kDecGroups decoder groups (group g decodes units it = g mod kDecGroups).
 // Roles spread over the four SM sub-partitions (warp w issues on SMSP w % 4,
 // which also hosts four decoder warps and one epilogue warp): the two
@@ -769,72 +840,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
       const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(2 * BPW * part);
       if (!(p.dbg & 1)) {
-        const uint32_t rec_s = smem_u32(rec);
-        const uint2 mw = lds_v2_u32(rec_s + kT2Mask + 8u * (32u * q + lane));
-        // 2-bit pair counts (the first SWAR step) give c0 of every band;
-        // 4-bit band counts as bytes: c[0] bands 0,2,4,6; c[1] 1,3,5,7;
-        // c[2] 8,10,12,14; c[3] 9,11,13,15
-        const uint32_t pl = mw.x - ((mw.x >> 1) & 0x55555555u);
-        const uint32_t ph = mw.y - ((mw.y >> 1) & 0x55555555u);
-        const uint32_t nl = (pl & 0x33333333u) + ((pl >> 2) & 0x33333333u);
-        const uint32_t nh = (ph & 0x33333333u) + ((ph >> 2) & 0x33333333u);
-        const uint32_t c[4] = {nl & 0x0F0F0F0Fu, (nl >> 4) & 0x0F0F0F0Fu, nh & 0x0F0F0F0Fu, (nh >> 4) & 0x0F0F0F0Fu};
-        uint32_t e[4] = {c[0], c[1], c[2], c[3]};
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {  // inclusive scan, byte lanes (<= 128)
-          uint32_t t[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) t[j] = __shfl_up_sync(0xffffffffu, e[j], d);
-          if ((int)lane >= d) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) e[j] += t[j];
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) e[j] -= c[j];
-        const uint32_t goff = q ? lds_u32(rec_s + 4u * (uint32_t)(q - 1)) : 0u;
-        const uint32_t vb = rec_s + kT2Val + 2u * goff;
-        const uint4 bo0 = lds_v4_u32(rec_s + kT2BandOff + 32u * q);
-        const uint4 bo1 = lds_v4_u32(rec_s + kT2BandOff + 32u * q + 16u);
-        const uint32_t bo[8] = {bo0.x, bo0.y, bo0.z, bo0.w, bo1.x, bo1.y, bo1.z, bo1.w};
-#pragma unroll
-        for (int pp = 0; pp < WPG / 4; ++pp) {  // this warp's part, unrolled so bands are compile-time
-          if (pp != part) continue;
-#pragma unroll
-        for (int c4 = 0; c4 < BPW / 4; ++c4) {  // 4 bands -> 8 TMEM columns
-          uint32_t packed[8];
-#pragma unroll
-          for (int i = 0; i < 4; i += 2) {
-            const int b = BPW * pp + 4 * c4 + i;  // bands b, b+1
-            // byte offsets of both bands' runs in 16-bit lanes: (prefix +
-            // band offset) * 2; byte prefixes are < 128, so sign-replicating
-            // selector nibbles give the zero bytes
-            const int j = (b & 7) >> 1;
-            const uint32_t pe = prmt(e[b >= 8 ? 2 : 0], e[b >= 8 ? 3 : 1],
-                                     (uint32_t)j | ((0x8u | j) << 4) | ((4u + j) << 8) | ((0x8u | j) << 12));
-            const uint32_t pr2 = pe + pe + (bo[b >> 1] + bo[b >> 1]);
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int bb = b + h;
-              const uint32_t r = h ? vb + (pr2 >> 16) : vb + (pr2 & 0xFFFFu);
-              const int sh = 4 * (bb & 7);
-              const uint32_t word = bb < 8 ? mw.x : mw.y;
-              // nibble -> table entry (8 bytes): selectors of both row pairs
-              // and the byte offset of pair 1's first value.  Absent elements
-              // need no predicate: the selectors pick zero bytes of the
-              // zero-extended loads.
-              const uint32_t nib8 = (sh >= 3 ? (word >> (sh - 3)) : (word << 3)) & 0x78u;
-              const uint2 ent = lds_v2_u32(lut_s | nib8);
-              const uint32_t r2 = r + (ent.x >> 16);
-              const uint32_t a0 = lds_u16z(r), a1 = lds_u16z(r + 2u);
-              const uint32_t b0 = lds_u16z(r2), b1 = lds_u16z(r2 + 2u);
-              packed[2 * (i + h)] = prmt(a0, a1, ent.x);
-              packed[2 * (i + h) + 1] = prmt(b0, b1, ent.y);
-            }
-          }
-          SALR_TMEM_ST_X8(taddr + 8u * c4, packed);
-        }
-        }
+        decode_tile_tb2(smem_u32(rec), taddr, q, lane, lut_s);
         tc_wait_st();
       }
       tc_fence_before();
@@ -1405,6 +1411,7 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t co
 }
 
 #include "salr_prefill.cuh"
+#include "salr_chain.cuh"
 
 static unsigned long long* g_trace = nullptr;  // set by salr_debug_set_trace (tools only)
 
@@ -1677,6 +1684,146 @@ int salr_debug_last_launch(int32_t* info12) {
 
 size_t salr_linear_workspace_zero_bytes(void) { return kUAccOff + kUAccBytes; }
 
+// ---- chain workspace: [sync counters][per-linear control + tickets + U] (zero
+// once) then the per-linear split-K partial tiles
+static constexpr size_t kChainSyncBytes = 4096;
+static constexpr size_t kChainCtrlBytes = 256, kChainTicketBytes = 64 * 1024;
+static constexpr size_t kChainLinBytes = kChainCtrlBytes + kChainTicketBytes + kUAccBytes;
+static constexpr size_t kChainZeroBytes = kChainSyncBytes + kMaxChain * kChainLinBytes;
+
+size_t salr_chain_workspace_zero_bytes(void) { return kChainZeroBytes; }
+
+size_t salr_chain_workspace_bytes(int64_t M, int L) {
+  const int bm = pick_bm(M < 1 ? 1 : M);
+  return kChainZeroBytes + (size_t)(L < 1 ? 1 : L) * align256((size_t)2 * sm_count() * bm * kTileN * 4);
+}
+
+int salr_chain_forward(const salr_chain_linear_t* lin, int L, const void* x0, int64_t M, int64_t ldx0,
+                       void* workspace, size_t workspace_bytes, int flags, void* stream) {
+  SALR_CHECK_ARG(lin != nullptr && L >= 1 && L <= kMaxChain, SALR_ERR_CONFIG, "chain length %d not in [1, %d]", L,
+                 kMaxChain);
+  SALR_CHECK_ARG(M >= 1 && M <= 256, SALR_ERR_SHAPE, "chain M=%lld not in [1, 256]", (long long)M);
+  SALR_CHECK_ARG(x0 && (reinterpret_cast<uintptr_t>(x0) & 15) == 0 && ldx0 % 8 == 0, SALR_ERR_SHAPE,
+                 "x0 must be 16-byte aligned with ldx0 a multiple of 8");
+  SALR_CHECK_ARG(workspace_bytes >= salr_chain_workspace_bytes(M, L), SALR_ERR_CONFIG, "workspace too small");
+  const int bm = pick_bm(M);
+  const int G = sm_count();
+  ChainParams cp = {};
+  ChainMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  cp.L = L;
+  cp.M = (int)M;
+  cp.n_mc = (int)((M + bm - 1) / bm);
+  cp.sync = reinterpret_cast<uint32_t*>(ws);
+  int ra_max = 0;
+  int64_t rec_max = 0;
+  const void* xl = x0;
+  int64_t ldxl = ldx0;
+  size_t poff = kChainZeroBytes;
+  for (int l = 0; l < L; ++l) {
+    const salr_chain_linear_t& d = lin[l];
+    SALR_CHECK_ARG(d.K >= 1 && d.N >= 1 && d.ldy >= d.N && d.ldy % 8 == 0 && d.y, SALR_ERR_SHAPE,
+                   "linear %d: invalid K=%lld N=%lld ldy=%lld", l, (long long)d.K, (long long)d.N, (long long)d.ldy);
+    SALR_CHECK_ARG(d.K % 8 == 0 && ldxl >= d.K, SALR_ERR_SHAPE, "linear %d: K=%lld must be a multiple of 8 and <= "
+                   "its input's width", l, (long long)d.K);
+    SALR_CHECK_ARG(d.r_pad == 0 || ((d.r_pad == 64 || d.r_pad == 128) && d.acat && d.bcat_t), SALR_ERR_CONFIG,
+                   "linear %d: r_pad must be 0, 64 or 128 with both factors", l);
+    ChainLin& c = cp.l[l];
+    c.records = d.records;
+    c.tile_off = d.tile_off;
+    c.y = d.y;
+    c.x = static_cast<const __nv_bfloat16*>(xl);
+    c.ldx = (int)ldxl;
+    c.acat = static_cast<const __nv_bfloat16*>(d.acat);
+    c.N = (int)d.N;
+    c.ldy = (int)d.ldy;
+    c.K = (int)d.K;
+    c.n_kt = (int)((d.K + kTileK - 1) / kTileK);
+    c.n_nt = (int)((d.N + kTileN - 1) / kTileN);
+    SALR_CHECK_ARG((int64_t)cp.n_mc * c.n_nt <= (int64_t)(kChainTicketBytes / 4) &&
+                       (int64_t)cp.n_mc * c.n_nt * c.n_kt < ((int64_t)1 << 31) &&
+                       M * (d.ldy > d.N ? d.ldy : d.N) < ((int64_t)1 << 31),
+                   SALR_ERR_SHAPE, "linear %d too large for the chain", l);
+    c.units = cp.n_mc * c.n_nt * c.n_kt;
+    c.ra = (int)(d.r_pad / 64);
+    uint8_t* blk = ws + kChainSyncBytes + (size_t)l * kChainLinBytes;
+    c.ctrl = reinterpret_cast<uint32_t*>(blk);
+    c.tickets = reinterpret_cast<uint32_t*>(blk + kChainCtrlBytes);
+    c.u_acc = reinterpret_cast<unsigned long long*>(blk + kChainCtrlBytes + kChainTicketBytes);
+    c.partials = reinterpret_cast<float*>(ws + poff);
+    poff += align256((size_t)2 * G * bm * kTileN * 4);
+    ra_max = std::max(ra_max, c.ra);
+    rec_max = std::max<int64_t>(rec_max, d.max_record_bytes > 0 ? d.max_record_bytes : kMaxRecordBytesT2);
+    int rc = make_map(&maps.x[l], xl, M, d.K, ldxl, bm);
+    if (rc) return rc;
+    if (c.ra) {
+      const int64_t n_pad = (int64_t)c.n_nt * kTileN;
+      if ((rc = make_map(&maps.b[l], d.bcat_t, n_pad, d.r_pad, d.r_pad, kTileN))) return rc;
+    } else {
+      maps.b[l] = maps.x[l];
+    }
+    xl = d.y;
+    ldxl = d.ldy;
+  }
+  // every CTA must own units of every linear (the split-K owner arithmetic
+  // assumes no empty CTA inside a tile's range): grid <= the smallest linear
+  int Gc = G;
+  for (int l = 0; l < L; ++l) Gc = std::min(Gc, cp.l[l].units);
+  cp.rec_slot = (uint32_t)((std::min<int64_t>(rec_max, kMaxRecordBytesT2) + 15) & ~15ll);
+  cp.stages = 8;
+  while (cp.stages > 4 && smem_plan(bm, cp.stages, ra_max, cp.rec_slot).total > kSmemMaxLinear) cp.stages -= 4;
+  const SmemPlan plan = smem_plan(bm, cp.stages, ra_max, cp.rec_slot);
+  SALR_CHECK_ARG(plan.total <= kSmemMaxLinear, SALR_ERR_CONFIG, "chain ring does not fit shared memory");
+  cp.x_off = plan.x_off;
+  cp.rec_off = plan.rec_off;
+  cp.ad_off = plan.ad_off;
+  cp.bar_off = plan.bar_off;
+  cp.trace = g_trace;
+  const bool pdl = (flags & SALR_FLAG_PDL) != 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto launch = [&](auto kern) -> int {
+    const int dev = cur_device();
+    static bool attr_done[kMaxDevices][4] = {};
+    const int slot = bm == 16 ? 0 : bm == 32 ? 1 : bm == 64 ? 2 : 3;
+    if (!attr_done[dev][slot]) {
+      SALR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMaxLinear));
+      attr_done[dev][slot] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)Gc);
+    cfg.blockDim = dim3(num_threads(4));
+    cfg.dynamicSmemBytes = plan.total;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    // every CTA waits on the others (Y counters, U slices): co-scheduled, or
+    // (programmatic launch, see SALR_FLAG_PDL) checked against occupancy
+    if (pdl) {
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, num_threads(4), plan.total) != cudaSuccess) {
+        (void)cudaGetLastError();
+        per_sm = 1;
+      }
+      SALR_CHECK_ARG(per_sm >= 1, SALR_ERR_CUDA, "chain grid cannot be co-resident");
+    } else {
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SALR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, maps, cp));
+    return SALR_OK;
+  };
+  switch (bm) {
+    case 16: return launch(salr_chain_kernel<16>);
+    case 32: return launch(salr_chain_kernel<32>);
+    case 64: return launch(salr_chain_kernel<64>);
+    default: return launch(salr_chain_kernel<128>);
+  }
+}
+
 size_t salr_linear_workspace_bytes(int64_t M, int64_t N, int64_t K, int64_t r_pad, int num_ctas) {
   return ws_layout(M, N, K, r_pad, num_ctas > 0 ? num_ctas : sm_count()).total;
 }
@@ -1782,7 +1929,8 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   p.u_mode = ra ? ((M <= 256 && ctas <= sm_count() && !(flags & SALR_FLAG_U_FP32)) ? 1 : 2) : 0;
   // cooperative split-tile reduction pays off once a partial tile has rows
   // to share (M >= 16); tiny ones stay with the last CTA (one round trip)
-  p.coop = (ctas <= sm_count() && M >= 16) ? 1 : 0;
+  static const bool no_coop = dbg_env("SALR_NO_COOP") != nullptr;
+  p.coop = (ctas <= sm_count() && M >= 16 && !no_coop) ? 1 : 0;
   {
     // Split tiles shared by exactly np (2..8) consecutive CTAs: make those a
     // thread-block cluster and reduce through DSMEM (no global round trips).

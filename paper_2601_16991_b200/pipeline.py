@@ -25,6 +25,7 @@ all ring capacities) are bit-identical for a given CTA count.
 
 from __future__ import annotations
 
+import ctypes
 import math
 import statistics
 from dataclasses import dataclass, field
@@ -245,6 +246,72 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
         xf = xb[:, : s.rows].float()
         out += ((xf @ tail.a_cat.float()) @ tail.b_cat.float()).to(out.dtype)
     return out
+
+
+_CHAIN_WS: dict = {}
+_CHAIN_TURN: dict = {}
+
+
+def _chain_workspace(M: int, L: int, device) -> torch.Tensor:
+    """Per-device chain scratch, two alternating buffers (as ``_workspace``)."""
+    need = int(_lib.load().salr_chain_workspace_bytes(M, L))
+    turn = _CHAIN_TURN.get(device.index, 0)
+    _CHAIN_TURN[device.index] = turn ^ 1
+    ws = _CHAIN_WS.get((device.index, turn))
+    if ws is None or ws.numel() < need:
+        for t in (0, 1):
+            _CHAIN_WS[(device.index, t)] = torch.zeros(need, dtype=torch.uint8, device=device)
+        ws = _CHAIN_WS[(device.index, turn)]
+    return ws
+
+
+def salr_chain(x, linears, outs, *, pdl: bool = False, workspace: torch.Tensor | None = None):
+    """A chain of SALR linears in ONE persistent launch: ``outs[0] = x @ W_0
+    [+ adapters]``, ``outs[l] = outs[l-1][:, :K_l] @ W_l [+ adapters]``
+    (bf16 outputs).  ``linears`` is a list of ``(BitmapSparseMatrix,
+    FusedAdapters | None)``, at most 4, M <= 256.  The weight stream runs
+    through the linear boundaries; only the next linear's X tiles wait for the
+    previous output (see csrc/salr_chain.cuh).  Results equal running
+    :func:`salr_linear` per linear on the same grid."""
+    _lib.require_cuda()
+    L = len(linears)
+    if not 1 <= L <= 4 or len(outs) != L:
+        raise ConfigError("a chain holds 1..4 linears and one output per linear")
+    xb, _ = _prep_x(x, linears[0][0].rows, False)
+    M = int(xb.shape[0])
+    if M > 256:
+        raise ConfigError("chained linears are decode-size (M <= 256)")
+    arr = (_lib.ChainLinear * L)()
+    keep = []
+    prev_n = None
+    for l, ((s, fused), y) in enumerate(zip(linears, outs)):
+        if not isinstance(s, BitmapSparseMatrix):
+            raise SalrError("chain entries must be BitmapSparseMatrix")
+        if y.shape != (M, s.cols) or y.dtype != torch.bfloat16 or not y.is_contiguous():
+            raise ShapeError(f"outs[{l}] must be a contiguous ({M}, {s.cols}) bfloat16 tensor")
+        if l and s.rows > prev_n:
+            raise ShapeError(f"linear {l} reads {s.rows} columns of a {prev_n}-column output")
+        if s.rows % 8:
+            raise ShapeError("chained linears need K a multiple of 8")
+        if fused is not None and fused.total_rank > 128:
+            raise ConfigError("chained linears take fused rank <= 128")
+        rec2, off2, mx = s.compute_format()
+        acat = bct = None
+        r_pad = 0
+        if fused is not None:
+            acat, bct = fused.device_operands()
+            r_pad = fused.r_pad
+        keep += [rec2, off2, acat, bct]
+        arr[l] = _lib.ChainLinear(_lib.ptr(rec2), _lib.ptr(off2), mx, s.rows, s.cols, _lib.ptr(acat),
+                                  _lib.ptr(bct), r_pad, _lib.ptr(y), s.cols)
+        prev_n = s.cols
+    ws = workspace if workspace is not None else _chain_workspace(M, L, xb.device)
+    global _launches
+    _launches += 1
+    _lib.check(_lib.load().salr_chain_forward(ctypes.addressof(arr), L, _lib.ptr(xb), M, int(xb.shape[1]),
+                                              _lib.ptr(ws), int(ws.numel()), _FLAG_PDL if pdl else 0,
+                                              _lib.stream_ptr()))
+    return outs
 
 
 def _check_probe(probe):

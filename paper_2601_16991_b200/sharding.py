@@ -126,8 +126,17 @@ class ShardedStack:
     current stream, so a whole step can be captured in one CUDA graph (NCCL
     collectives are graph-capturable); ``world == 1`` skips the gathers."""
 
-    def __init__(self, layers, plan, world: int = 1, rank: int = 0, group=None, tokens: int = 1):
+    def __init__(self, layers, plan, world: int = 1, rank: int = 0, group=None, tokens: int = 1,
+                 chain: bool | None = None):
         self.layers, self.plan, self.world, self.rank, self.group = layers, list(plan), world, rank, group
+        # chain=True runs a layer as one persistent launch (salr_chain; single
+        # GPU, decode-size M, each linear reading leading columns of the
+        # previous output).  Off by default: measured slower than per-linear
+        # launches (DESIGN.md 4.4 -- the split-K tails become L2 round trips
+        # under the next linear's weight stream and gate every CTA).
+        ok = world == 1 and tokens <= 256 and len(self.plan) <= 4 and all(
+            keep is None or keep[0] == 0 for _, keep in self.plan[1:])
+        self.chain = bool(chain) and ok
         first = layers[0][self.plan[0][0]]
         dev = first.s.device
         self.x_in = torch.zeros(tokens, first.s.rows, dtype=torch.bfloat16, device=dev)
@@ -142,6 +151,8 @@ class ShardedStack:
         return gather_columns(y, lin.n, group=self.group, keep=keep)
 
     def step(self, x):
+        if self.chain:
+            return self._step_chain(x)
         h = x
         launches = 0
         for li, layer in enumerate(self.layers):
@@ -152,4 +163,16 @@ class ShardedStack:
                 keep = self.plan[j + 1][1] if j + 1 < len(self.plan) else self.plan[0][1]
                 h = self._next_input(y, lin, keep)
         self.launches_per_step = launches
+        return h
+
+    def _step_chain(self, x):
+        from .pipeline import salr_chain
+        h = x
+        for li, layer in enumerate(self.layers):
+            outs = [self.bufs[name][li & 1] for name, _ in self.plan]
+            salr_chain(h, [(layer[name].s, layer[name].f) for name, _ in self.plan], outs, pdl=True)
+            last = outs[-1]
+            keep = self.plan[0][1]
+            h = last if keep is None else last[:, keep[0]:keep[1]]
+        self.launches_per_step = len(self.layers)
         return h
