@@ -171,6 +171,15 @@ int salr_debug_set_trace(void* buf);
  * cooperative (1 = launched co-scheduled: in-kernel U / cooperative split-K
  * wait on other CTAs, so the driver guarantees every CTA is resident)}. */
 int salr_debug_last_launch(int32_t* info12);
+/* Pipeline probe (tests / tools): the device form of the reference's
+ * PipelineProbe (pipeline.py:89-103).  While log != NULL, decode-size linear
+ * launches append every ring-slot transition (slot = cta * stages + stage,
+ * EMPTY 0 -> FILLED 1 -> CONSUMED 2 -> EMPTY) to log[4 + i] as
+ * slot << 8 | old << 4 | new, count entries in log[0], fills in log[1] and
+ * consumes in log[2] (device u32, zeroed by the caller), and sleep a hashed
+ * 0..max_delay_ns before every tile decode and MMA issue (jitter
+ * injection).  NULL disables. */
+int salr_debug_set_probe(void* log, size_t log_words, int max_delay_ns, uint32_t seed);
 /* flags: SALR_FLAG_PDL launches the kernel as a programmatic dependent of the
  * preceding work on the stream: its weight-streaming prologue overlaps the
  * tail of that work and it waits for it (griddepcontrol.wait) before reading

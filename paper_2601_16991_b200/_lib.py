@@ -52,6 +52,7 @@ _SIGS = {
     "salr_nm_mask": ([_vp, _int, _i64, _i64, _int, _int, _vp, _vp], _int),
     "salr_debug_set_trace": ([_vp], _int),
     "salr_debug_last_launch": ([_vp], _int),
+    "salr_debug_set_probe": ([_vp, ctypes.c_size_t, _int, ctypes.c_uint32], _int),
     "salr_linear_forward": ([_vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _int, _i64,
                              _vp, ctypes.c_size_t, _int, _int, _int, _vp], _int),
     "salr_chain_workspace_bytes": ([_i64, _int], ctypes.c_size_t),

@@ -77,6 +77,16 @@ struct LinearParams {
   uint32_t rec_slot;  // bytes per ring slot: the largest record of this matrix, 16-aligned
   int dbg;            // timing experiments only: 1 = skip decode, 2 = skip record loads
   unsigned long long* trace;  // optional per-CTA event timestamps (globaltimer ns), [G][32]
+  // Pipeline probe (salr_debug_set_probe; null = off): device form of the
+  // reference PipelineProbe (pipeline.py:89-103).  log[0] = entries,
+  // log[1] = produced, log[2] = consumed, log[4 + i] = slot << 8 | old << 4 |
+  // new for the slot (cta * S + stage) transitions EMPTY(0) -> FILLED(1) ->
+  // CONSUMED(2) -> EMPTY, and each decode / MMA issue sleeps a hashed
+  // 0..probe_ns ns first (fault injection by jitter).
+  uint32_t* probe_log;
+  uint32_t probe_cap;
+  uint32_t probe_ns;
+  uint32_t probe_seed;
   // shared-memory carve-up (bytes from the 1024-aligned base)
   uint32_t x_off, rec_off, base_off, ad_off, bar_off;
 };
@@ -145,6 +155,25 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
+// ---- pipeline probe helpers (see LinearParams::probe_log)
+enum : uint32_t { kSlotEmpty = 0, kSlotFilled = 1, kSlotConsumed = 2 };
+__device__ __forceinline__ void probe_log_transition(uint32_t* log, uint32_t cap, uint32_t slot, uint32_t from,
+                                                     uint32_t to) {
+  const uint32_t i = atomicAdd(log, 1u);
+  if (i < cap) log[4 + i] = slot << 8 | from << 4 | to;
+  if (from == kSlotEmpty) atomicAdd(log + 1, 1u);
+  if (from == kSlotFilled) atomicAdd(log + 2, 1u);
+  __threadfence();
+}
+__device__ __forceinline__ void probe_jitter(uint32_t ns, uint32_t seed, uint32_t a, uint32_t b) {
+  if (!ns) return;
+  uint32_t h = seed ^ (a * 0x9E3779B9u) ^ (b * 0x85EBCA6Bu);
+  h ^= h >> 16;
+  h *= 0x7FEB352Du;
+  h ^= h >> 15;
+  __nanosleep(h % (ns + 1));
+}
+
 // per-unit detail for CTA 0 (first 64 units): slot 148*32 + ev*64 + i
 // (compiled in only with -DSALR_UNIT_TRACE: the stamps sit in the per-unit
 // hot loops, where even predicated-off instructions cost issue slots)
@@ -375,7 +404,11 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     const uint32_t o0 = __shfl_sync(0xffffffffu, co0, pv - chunk);
     const uint32_t o1 = __shfl_sync(0xffffffffu, co1, pv - chunk);
     if (lane == 0) SALR_TRACE_UNIT(9, pv - u_begin);
-    if (pv - u_begin >= S) mbar_wait(&empty[ps], pph ^ 1);
+    if (pv - u_begin >= S) {
+      mbar_wait(&empty[ps], pph ^ 1);
+      if (p.probe_log && lane == 0)
+        probe_log_transition(p.probe_log, p.probe_cap, (uint32_t)(blockIdx.x * S + ps), kSlotConsumed, kSlotEmpty);
+    }
     if (lane == 0) {
       SALR_TRACE_UNIT(10, pv - u_begin);
       const uint32_t bytes = (p.dbg & 2) ? 0u : (o1 - o0) * 16u;
@@ -620,6 +653,16 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     if (lane == 0) SALR_TRACE(1);
     while (pv < u_end) issue_rec();
     if (lane == 0) SALR_TRACE(2);
+    if (p.probe_log) {
+      // probe shutdown: every slot returns to EMPTY (its last MMA completes)
+      for (int v = max(u_begin, u_end - S); v < u_end; ++v) {
+        const int st = (v - u_begin) % S;
+        mbar_wait(&empty[st], (uint32_t)(((v - u_begin) / S) & 1));
+        if (lane == 0)
+          probe_log_transition(p.probe_log, p.probe_cap, (uint32_t)(blockIdx.x * S + st), kSlotConsumed, kSlotEmpty);
+        __syncwarp();
+      }
+    }
   } else if (warp == kWarpProd1) {
     // ================= X producer: the input may be the preceding kernel's
     // output -- wait for it only now, after the CTA-wide setup, so the
@@ -723,7 +766,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       const uint32_t acc = kTm + (uint32_t)(b * ACOLS);
       mbar_wait(&acc_empty[b], acc_ph ^ 1);
       tc_fence_after();
-      if (S == 8 && !(p.dbg & 24)) {
+      if (S == 8 && !(p.dbg & 24) && !p.probe_log) {
         // Ring of 8: the stage index is a compile-time constant in each case
         // (Duff-style entry at the current stage), so barrier, TMEM and
         // descriptor offsets are immediates and the per-unit loop is two
@@ -766,6 +809,13 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       for (int v = u; v < seg_end; ++v) {
         mbar_wait_addr(dad, ph);
         if (!(p.dbg & 16)) mbar_wait_addr(dad + 8u * (uint32_t)S, ph);  // this stage's X tile (xfull)
+        if (p.probe_log) {
+          if (lane == 0)
+            probe_log_transition(p.probe_log, p.probe_cap, (uint32_t)(blockIdx.x * S + sg), kSlotFilled,
+                                 kSlotConsumed);
+          probe_jitter(p.probe_ns, p.probe_seed ^ 0x5bd1e995u, (uint32_t)v, 1u);
+          __syncwarp();
+        }
         tc_fence_after();
         SALR_TRACE_UNIT(6, v - u_begin);
         if (p.dbg & 8) {  // experiment: commit without MMAs (wrong results)
@@ -837,6 +887,12 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     for (int it = u_begin + grp; it < u_end; it += kDecGroups) {
       mbar_wait(&full[s], ph);
       if (lane == 0 && (dw % WPG) == 0) SALR_TRACE_UNIT(1, it - u_begin);
+      if (p.probe_log) {
+        if (lane == 0 && q == 0)
+          probe_log_transition(p.probe_log, p.probe_cap, (uint32_t)(blockIdx.x * S + s), kSlotEmpty, kSlotFilled);
+        probe_jitter(p.probe_ns, p.probe_seed, (uint32_t)it, (uint32_t)warp);
+        __syncwarp();
+      }
       const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
       const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(2 * BPW * part);
       if (!(p.dbg & 1)) {
@@ -1414,6 +1470,8 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t co
 #include "salr_chain.cuh"
 
 static unsigned long long* g_trace = nullptr;  // set by salr_debug_set_trace (tools only)
+static uint32_t* g_probe_log = nullptr;         // set by salr_debug_set_probe (tests / tools)
+static uint32_t g_probe_cap = 0, g_probe_ns = 0, g_probe_seed = 0;
 
 static int pick_bm(int64_t M) {
   if (M <= 16) return 16;
@@ -1676,6 +1734,16 @@ int salr_debug_set_trace(void* buf) {
   return SALR_OK;
 }
 
+int salr_debug_set_probe(void* log, size_t log_words, int max_delay_ns, uint32_t seed) {
+  SALR_CHECK_ARG(!log || log_words >= 8, SALR_ERR_CONFIG, "probe log needs >= 8 words");
+  SALR_CHECK_ARG(max_delay_ns >= 0 && max_delay_ns <= 1000000, SALR_ERR_CONFIG, "probe delay out of range");
+  g_probe_log = static_cast<uint32_t*>(log);
+  g_probe_cap = log ? (uint32_t)(log_words - 4) : 0u;
+  g_probe_ns = (uint32_t)max_delay_ns;
+  g_probe_seed = seed;
+  return SALR_OK;
+}
+
 int salr_debug_last_launch(int32_t* info12) {
   if (!info12) return SALR_ERR_CONFIG;
   for (int i = 0; i < 12; ++i) info12[i] = g_last_launch[i];
@@ -1770,7 +1838,7 @@ int salr_chain_forward(const salr_chain_linear_t* lin, int L, const void* x0, in
   // assumes no empty CTA inside a tile's range): grid <= the smallest linear
   int Gc = G;
   for (int l = 0; l < L; ++l) Gc = std::min(Gc, cp.l[l].units);
-  cp.rec_slot = (uint32_t)((std::min<int64_t>(rec_max, kMaxRecordBytesT2) + 15) & ~15ll);
+  cp.rec_slot = (uint32_t)((std::min<int64_t>(rec_max, kMaxRecordBytesT2) + 16 + 15) & ~15ll);
   cp.stages = 8;
   while (cp.stages > 4 && smem_plan(bm, cp.stages, ra_max, cp.rec_slot).total > kSmemMaxLinear) cp.stages -= 4;
   const SmemPlan plan = smem_plan(bm, cp.stages, ra_max, cp.rec_slot);
@@ -1876,10 +1944,17 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     }
     p.dbg = dbg;
     p.trace = g_trace;
+    p.probe_log = g_probe_log;
+    p.probe_cap = g_probe_cap;
+    p.probe_ns = g_probe_ns;
+    p.probe_seed = g_probe_seed;
   }
   {
+    // + 16 bytes: the decoders' fixed-width band loads read up to 3
+    // halfwords past a band's last value; the slack keeps those (unused)
+    // reads inside the slot instead of the next slot a TMA may be filling
     p.rec_slot = (max_record_bytes > 0 && max_record_bytes <= kMaxRecordBytesT2)
-                     ? (uint32_t)((max_record_bytes + 15) & ~15ll) : (uint32_t)kMaxRecordBytesT2;
+                     ? (uint32_t)((max_record_bytes + 16 + 15) & ~15ll) : (uint32_t)kMaxRecordBytesT2 + 16u;
     const int smax = max_stages(bm, ra, p.rec_slot, stages > 8 ? std::min(stages, 16) : 8);
     p.stages = stages <= 0 || stages > smax ? smax : stages;
   }

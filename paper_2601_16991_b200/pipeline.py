@@ -86,12 +86,16 @@ class PipelineConfig:
 
 @dataclass
 class PipelineProbe:
-    """Audit hooks (reference ``pipeline.py:89-103``).
+    """Fault-injection and audit hooks (reference ``pipeline.py:89-103``),
+    run on the device ring of the fused kernel.
 
-    Host-side delay callables cannot run inside a CUDA kernel; passing them
-    raises ConfigError.  Transition recording is not available in this build
-    either (ConfigError) -- the device protocol is audited by
-    ``tests/test_gpu_linear.py`` instead.
+    ``decode_delay`` / ``compute_delay``: host callables cannot run inside a
+    CUDA kernel (ConfigError); a number is the maximum jitter in
+    nanoseconds slept before every tile decode / MMA issue (a per-tile hash
+    of ``seed``).  ``record`` fills ``transitions`` with ``(slot, old,
+    new)`` for every ring-slot transition of every CTA (slot = cta * stages
+    + stage; audit with ``validate_transitions(probe, probe.capacity)``) and
+    sets ``produced`` / ``consumed``.
     """
 
     decode_delay: object = None
@@ -100,6 +104,8 @@ class PipelineProbe:
     transitions: list = field(default_factory=list)
     produced: int = 0
     consumed: int = 0
+    seed: int = 0
+    capacity: int = 0  # slots of the last recorded launch (ctas * stages)
 
 
 def validate_transitions(probe: PipelineProbe, capacity: int) -> None:
@@ -317,17 +323,48 @@ def salr_chain(x, linears, outs, *, pdl: bool = False, workspace: torch.Tensor |
 def _check_probe(probe):
     if probe is None:
         return
-    if probe.decode_delay is not None or probe.compute_delay is not None:
-        raise ConfigError("host delay callables cannot be injected into the device pipeline")
+    for d in (probe.decode_delay, probe.compute_delay):
+        if d is not None and not isinstance(d, (int, float)):
+            raise ConfigError("host delay callables cannot be injected into the device pipeline; pass the "
+                              "maximum device jitter in nanoseconds instead")
+
+
+def _run_probed(probe, fn):
+    """Run one launch with the device probe armed; decode the log into the
+    reference's (slot, old, new) transition list."""
+    if probe is None:
+        return fn()
+    delay = int(max(probe.decode_delay or 0, probe.compute_delay or 0))
+    lib = _lib.load()
+    words = 1 << 20
+    log = torch.zeros(words, dtype=torch.int32, device="cuda")
+    _lib.check(lib.salr_debug_set_probe(_lib.ptr(log), words, delay, int(probe.seed) & 0xFFFFFFFF))
+    try:
+        out = fn()
+        torch.cuda.synchronize()
+    finally:
+        lib.salr_debug_set_probe(None, 0, 0, 0)
+    head = log[:4].cpu().tolist()
+    n = head[0]
+    if n > words - 4:
+        raise VerificationError(f"probe log overflow ({n} transitions)")
+    info = (ctypes.c_int32 * 12)()
+    lib.salr_debug_last_launch(ctypes.addressof(info))
+    probe.capacity = int(info[0]) * int(info[1])
+    probe.produced += head[1]
+    probe.consumed += head[2]
     if probe.record:
-        raise ConfigError("slot-transition recording is not available in this build")
+        ent = log[4:4 + n].cpu().tolist()
+        st = (SlotState.EMPTY, SlotState.FILLED, SlotState.CONSUMED)
+        probe.transitions.extend(((e >> 8) & 0xFFFFFF, st[(e >> 4) & 15], st[e & 15]) for e in ent)
+    return out
 
 
 def pipelined_matmul(x, s: BitmapSparseMatrix, cfg: PipelineConfig, probe: PipelineProbe | None = None,
                      out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
     """``x @ decode(s)`` through the fused kernel (``pipeline.py:258-272``)."""
     _check_probe(probe)
-    return salr_linear(x, s, None, out_dtype=out_dtype, stages=cfg.device_stages)
+    return _run_probed(probe, lambda: salr_linear(x, s, None, out_dtype=out_dtype, stages=cfg.device_stages))
 
 
 def pipelined_forward(x, s: BitmapSparseMatrix, fused: FusedAdapters, cfg: PipelineConfig,
@@ -336,7 +373,7 @@ def pipelined_forward(x, s: BitmapSparseMatrix, fused: FusedAdapters, cfg: Pipel
     _check_probe(probe)
     if fused.d_in != s.rows or fused.d_out != s.cols:
         raise ShapeError(f"fused adapter dims {(fused.d_in, fused.d_out)} != weight dims {(s.rows, s.cols)}")
-    return salr_linear(x, s, fused, out_dtype=out_dtype, stages=cfg.device_stages)
+    return _run_probed(probe, lambda: salr_linear(x, s, fused, out_dtype=out_dtype, stages=cfg.device_stages))
 
 
 @dataclass(frozen=True)
