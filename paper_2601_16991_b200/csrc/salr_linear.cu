@@ -102,11 +102,12 @@ constexpr int kCtrlEpoch = 0, kCtrlDone = 1, kCtrlReady = 2, kCtrlUsed = 4, kCtr
 constexpr int kUSlice = 64;  // K rows per dynamically claimed U slice
 constexpr int kDoneTicketOff = 16 * 1024;  // second counter per split tile (workspace ticket area)
 constexpr int kUAccElems = 256 * 128;  // per parity buffer: M <= 256 rows x r_pad <= 128
-// Warp layout for NG decoder groups of four warps (one per TMEM lane quarter):
-// warps 0-3 producers / MMA / publisher, 4 .. 4+4NG-1 decoders, then four
-// epilogue warps.
+constexpr int kNumDecWarps = 16;
+constexpr int kNumThreads = 800;               // 25 warps
 constexpr int kFirstDecWarp = 4;
-__host__ __device__ constexpr int num_dec_warps(int ng) { return 4 * ng; }
+constexpr int kFirstEpiWarp = 20;
+// warp layout helpers of the chained-linear kernel (salr_chain.cuh): NG
+// decoder groups of four warps after warps 0-3, then four epilogue warps
 __host__ __device__ constexpr int first_epi_warp(int ng) { return kFirstDecWarp + 4 * ng; }
 __host__ __device__ constexpr int num_threads(int ng) { return 32 * (first_epi_warp(ng) + 4); }
 constexpr uint32_t kAdTileBytes = 128 * 128;   // B_cat^T tile: 128 rows x 64 bf16
@@ -236,8 +237,11 @@ __device__ __forceinline__ uint32_t ticket_add_acq_rel(uint32_t* addr, uint32_t 
 // driven by the nibble table expand the 4 rows -- no per-element rank
 // popcounts.  Writes the lane's 32 bf16-pair columns of the A operand with
 // tcgen05.st (the caller waits and fences).
+// (BPW < 16: bands [BPW * part, BPW * part + BPW) only, a decoder group of
+// more than four warps splitting the rows; taddr then points at that part.)
+template <int BPW = 16>
 __device__ __forceinline__ void decode_tile_tb2(uint32_t rec_s, uint32_t taddr, int q, uint32_t lane,
-                                                uint32_t lut_s) {
+                                                uint32_t lut_s, int part = 0) {
   const uint2 mw = lds_v2_u32(rec_s + kT2Mask + 8u * (32u * q + lane));
   // 4-bit band counts as bytes: c[0] bands 0,2,4,6; c[1] 1,3,5,7;
   // c[2] 8,10,12,14; c[3] 9,11,13,15
@@ -265,11 +269,14 @@ __device__ __forceinline__ void decode_tile_tb2(uint32_t rec_s, uint32_t taddr, 
   const uint4 bo1 = lds_v4_u32(rec_s + kT2BandOff + 32u * q + 16u);
   const uint32_t bo[8] = {bo0.x, bo0.y, bo0.z, bo0.w, bo1.x, bo1.y, bo1.z, bo1.w};
 #pragma unroll
-  for (int c4 = 0; c4 < 4; ++c4) {  // 4 bands -> 8 TMEM columns
+  for (int pp = 0; pp < 16 / BPW; ++pp) {  // this warp's part, unrolled so bands are compile-time
+    if (pp != part) continue;
+#pragma unroll
+  for (int c4 = 0; c4 < BPW / 4; ++c4) {  // 4 bands -> 8 TMEM columns
     uint32_t packed[8];
 #pragma unroll
     for (int i = 0; i < 4; i += 2) {
-      const int b = 4 * c4 + i;  // bands b, b+1
+      const int b = BPW * pp + 4 * c4 + i;  // bands b, b+1
       // byte offsets of both bands' runs in 16-bit lanes: (prefix + band
       // offset) * 2; byte prefixes are < 128, so sign-replicating selector
       // nibbles give the zero bytes
@@ -297,30 +304,22 @@ __device__ __forceinline__ void decode_tile_tb2(uint32_t rec_s, uint32_t taddr, 
     }
     SALR_TMEM_ST_X8(taddr + 8u * c4, packed);
   }
+  }
 }
 
 // kDecGroups decoder groups (group g decodes units it = g mod kDecGroups).
-// Roles spread over the four SM sub-partitions (warp w issues on SMSP w % 4,
-// which also hosts four decoder warps and one epilogue warp): the two
-// producers on SMSPs 0 and 3, the MMA issuer on 1, the publisher on 2.  The
-// producers and the MMA warp are the per-unit serial path of the CTA, so no
-// two of them share a sub-partition.
-constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPub = 2;
-constexpr int kWarpProd1 = 3;
+constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPub = 2;  // warp 3 idle
+constexpr int kWarpProd1 = 24;
 
-template <int BM, int kDecGroups>
-__global__ void __launch_bounds__(num_threads(kDecGroups), 1)
+template <int BM, int kDecGroups, bool kProbe = false>
+__global__ void __launch_bounds__(kNumThreads, 1)
     salr_linear_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
                        const __grid_constant__ CUtensorMap uhimap, const __grid_constant__ CUtensorMap ulomap,
                        const LinearParams p) {
   constexpr int NACC = nacc_for(BM);
   constexpr int ACOLS = acc_cols_for(BM);
   constexpr uint32_t IDESC = idesc_bf16_f32(128, BM);
-  constexpr int kNumDecWarps = num_dec_warps(kDecGroups);
-  constexpr int kFirstEpiWarp = first_epi_warp(kDecGroups);
-  constexpr int kNumThreads = num_threads(kDecGroups);
-  constexpr int kUWide = 32 * (kNumDecWarps + 4);  // decoder + epilogue threads (wide U path)
-  constexpr int WPG = 4;                          // decoder warps per group: one per lane quarter
+  constexpr int WPG = kNumDecWarps / kDecGroups;  // decoder warps per group
   constexpr int RPW = 4 * kTileK / WPG;           // rows per decoder warp (all 4 lane quarters per group)
 
   extern __shared__ uint8_t smem_raw[];
@@ -368,16 +367,20 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
   const bool early_split = !p.cluster && (u_begin % p.n_kt != 0 || first_seg_end0 - u_begin < p.n_kt) &&
                            first_seg_end0 < u_end;
 
-  // ---- producers.  kWarpProd0 streams the weight records of every unit,
-  // kWarpProd1 the X tiles: each loop is the minimum per unit (wait for the
-  // stage to drain, one elected copy), since the producers sit on the CTA's
-  // serial path and share their SM sub-partitions with busy decoder warps.
+  // ---- producer state (warps kWarpProd0 / kWarpProd1, units of one parity).
   // Record offsets are fetched 32 units at a time, one chunk ahead, one
   // coalesced load per lane, so the issue loop never waits on a global load.
+  // Each multi-instance role owns the stages s = instance (mod instances), so
+  // an instance never waits on a stage two phases ahead (mbarrier parity
+  // waits cannot tell those apart): the host picks S as a multiple of the
+  // decoder group count, and the producers / row-base warps run as pairs only
+  // when S is even.
+  const int NP = (S % 2 == 0) ? 2 : 1;
+  const int pk = warp == kWarpProd1 ? 1 : 0;
   uint32_t co0 = 0, co1 = 0, no0 = 0, no1 = 0;
   int chunk = u_begin;
-  int pv = u_begin;  // next unit to issue
-  int ps = 0;        // its stage
+  int pv = u_begin + pk;  // next unit to issue (this producer's parity)
+  int ps = pk;            // < S whenever this producer is active
   uint32_t pph = 0;
   const uint64_t pol_stream = l2_policy_evict_first();
   auto load_chunk = [&](int c0, uint32_t& o0, uint32_t& o1) {
@@ -389,13 +392,21 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       o1 = __ldg(p.tile_off + t + 1);
     }
   };
-  // Record of unit pv into its stage.  The copy goes out before
-  // arrive.expect_tx (the phase cannot complete before the arrive, and
-  // issuing the copy first keeps it off the arrive's latency).  The first
-  // ring's worth of units never waits for `empty`.
-  auto issue_rec = [&]() {
+  // X tile of unit v into stage st (the input; may have to wait for the
+  // preceding kernel under programmatic dependent launch)
+  auto issue_x = [&](int v, int st) {
+    const int kt = v % p.n_kt;
+    const int mc = v / tiles_per_mc;
+    tma_2d_g2s(xbuf + (size_t)st * BM * 128, &xmap, kt * kTileK, mc * BM, &xfull[st]);
+    mbar_arrive_expect_tx(&xfull[st], BM * 128);
+  };
+  // Issue unit pv.  The copies go out before arrive.expect_tx (the phase
+  // cannot complete before the arrive, and issuing the copy first keeps it
+  // off the arrive's latency).  The first ring's worth of units never waits
+  // for `empty`.  with_x = false defers the X tile (see the PDL prologue).
+  auto issue_one = [&](bool with_x) {
     if (lane == 0) SALR_TRACE_UNIT(8, pv - u_begin);
-    if (pv - chunk >= 32) {
+    while (pv - chunk >= 32) {
       chunk += 32;
       co0 = no0;
       co1 = no1;
@@ -406,7 +417,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     if (lane == 0) SALR_TRACE_UNIT(9, pv - u_begin);
     if (pv - u_begin >= S) {
       mbar_wait(&empty[ps], pph ^ 1);
-      if (p.probe_log && lane == 0)
+      if (kProbe && lane == 0)
         probe_log_transition(p.probe_log, p.probe_cap, (uint32_t)(blockIdx.x * S + ps), kSlotConsumed, kSlotEmpty);
     }
     if (lane == 0) {
@@ -414,18 +425,19 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       const uint32_t bytes = (p.dbg & 2) ? 0u : (o1 - o0) * 16u;
       if (bytes) bulk_g2s_hint(recbuf + (size_t)ps * p.rec_slot, p.records + (size_t)o0 * 16u, bytes, &full[ps], pol_stream);
       mbar_arrive_expect_tx(&full[ps], bytes);
+      if (with_x && !(p.dbg & 16)) issue_x(pv, ps);
       SALR_TRACE_UNIT(0, pv - u_begin);
     }
     __syncwarp();
-    if (++ps == S) { ps = 0; pph ^= 1; }
-    ++pv;
+    ps += NP;
+    if (ps >= S) { ps -= S; pph ^= 1; }
+    pv += NP;
   };
 
+  const bool producer = warp == kWarpProd0 || (warp == kWarpProd1 && NP == 2);
   if (warp == kWarpProd0 || warp == kWarpProd1) {
-    if (warp == kWarpProd0) {
-      load_chunk(u_begin, co0, co1);
-      load_chunk(u_begin + 32, no0, no1);
-    }
+    load_chunk(u_begin, co0, co1);
+    load_chunk(u_begin + 32, no0, no1);
     if (warp == kWarpProd0 && lane == 0) {
       prefetch_tmap(&xmap);
       if (p.ra) {
@@ -436,7 +448,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       for (int s = 0; s < S; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&xfull[s], 1);
-        mbar_init(&empty[s], 1);  // the MMA commit: decode and X tile of the stage consumed
+        mbar_init(&empty[s], 1);
         mbar_init(&decoded[s], WPG);
       }
       for (int b = 0; b < 2; ++b) {
@@ -450,13 +462,12 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     }
     named_bar_sync(2, 64);  // barriers initialised before either producer uses them
     if (threadIdx.x == 0) SALR_TRACE(21);
-    // Start streaming before the CTA-wide setup barrier: the first ring's
-    // worth of records of the first output tile (never blocks).
-    if (warp == kWarpProd0) {
-      const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
-      const int pre = min(first_seg_end, u_begin + S);
-      while (pv < pre) issue_rec();
-    }
+    // Start streaming before the CTA-wide setup barrier: this producer's share
+    // of the first ring's worth of units of the first output tile (never blocks).
+    const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
+    const int pre = min(first_seg_end, u_begin + S);
+    if (producer)
+      while (pv < pre) issue_one(false);
     if (threadIdx.x == 0) SALR_TRACE(23);
   }
   // ---- in-kernel U (u_mode 1) geometry.  K is cut into slices of kUSlice
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     if (warp >= (wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4 && u_staged_fn()) {
       const int ut = (warp - (wide ? kFirstDecWarp : kFirstEpiWarp)) * 32 + (int)lane;
       const int nsl = (p.K + kUSlice - 1) / kUSlice;
-      if ((int)blockIdx.x < nsl) u_load_a((int)blockIdx.x, ut, wide ? kUWide : 128);
+      if ((int)blockIdx.x < nsl) u_load_a((int)blockIdx.x, ut, wide ? 640 : 128);
       const int pf = G + (int)blockIdx.x;  // a slice another CTA may claim
       if (ut == 0 && pf < nsl)
         prefetch_l2_bulk(p.acat + (size_t)pf * kUSlice * 64 * p.ra,
@@ -499,7 +510,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
   // nibble table of the decoders: static shared memory, so its address is a
   // compile-time constant folded into the decoders' loads
   __shared__ __align__(128) uint64_t s_lut[16];
-  if (warp == kWarpPub && lane < 16) s_lut[lane] = nib_lut_entry(lane);
+  if (warp == 3 && lane < 16) s_lut[lane] = nib_lut_entry(lane);
   const uint32_t lut_s = smem_u32(s_lut);
   if (warp == kWarpMma) {
     tmem_alloc(tmem_slot, 512);
@@ -522,7 +533,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
   // delay; measured: with 16 units per CTA the decoders are better off
   // starting to decode).
   const bool u_wide = u_geom_wide();
-  const int kUThreads = u_wide ? kUWide : 128;
+  const int kUThreads = u_wide ? 640 : 128;
   if (p.u_mode == 1 && warp >= (u_wide ? kFirstDecWarp : kFirstEpiWarp) && warp < kFirstEpiWarp + 4) {
     const int ut = (warp - (u_wide ? kFirstDecWarp : kFirstEpiWarp)) * 32 + (int)lane;
     const int rp = 64 * p.ra;
@@ -647,15 +658,29 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     if (ut == 0 && done) SALR_TRACE(13);
   }
 
-  if (warp == kWarpProd0) {
-    // ================= record producer: weights never depend on the
-    // preceding kernel, so it streams on without waiting for it
-    if (lane == 0) SALR_TRACE(1);
-    while (pv < u_end) issue_rec();
-    if (lane == 0) SALR_TRACE(2);
-    if (p.probe_log) {
-      // probe shutdown: every slot returns to EMPTY (its last MMA completes)
+  if (warp == kWarpProd0 || warp == kWarpProd1) {
+    // ================= TMA producers.  Weights never depend on the preceding
+    // kernel; the input X may (it can be that kernel's output): wait for it
+    // only now -- after the CTA-wide setup, so the decoders already work on
+    // the first ring -- then send the X tiles of the units already in flight.
+    pdl_wait();
+    if (threadIdx.x == 0) SALR_TRACE(24);
+    if (lane == 0 && producer) {
+      const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
+      const int pre = min(first_seg_end, u_begin + S);
+      if (!(p.dbg & 16))
+        for (int v = u_begin + pk; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) SALR_TRACE(28);
+    if (lane == 0 && pk == 0) SALR_TRACE(1);
+    if (producer)
+      while (pv < u_end) issue_one(true);
+    if (kProbe && producer) {
+      // probe shutdown: every slot of this producer returns to EMPTY (its
+      // last MMA completes)
       for (int v = max(u_begin, u_end - S); v < u_end; ++v) {
+        if ((v - u_begin) % NP != pk) continue;
         const int st = (v - u_begin) % S;
         mbar_wait(&empty[st], (uint32_t)(((v - u_begin) / S) & 1));
         if (lane == 0)
@@ -663,37 +688,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
         __syncwarp();
       }
     }
-  } else if (warp == kWarpProd1) {
-    // ================= X producer: the input may be the preceding kernel's
-    // output -- wait for it only now, after the CTA-wide setup, so the
-    // decoders already work on the first ring.  (k-tile, m-chunk) advance
-    // without divisions.  Both producers wait for the same `empty` phase (the
-    // MMA commit of the stage's previous unit), so an X tile never lands in
-    // a stage whose previous X tile an MMA may still read.
-    pdl_wait();
-    if (threadIdx.x == 32 * kWarpProd1) SALR_TRACE(24);
-    int kt = u_begin % p.n_kt, mc = u_begin / tiles_per_mc, rem = tiles_per_mc - u_begin % tiles_per_mc;
-    int xs = 0;
-    uint32_t xph = 0;
-    for (int v = u_begin; v < u_end; ++v) {
-      if (v - u_begin >= S) mbar_wait(&empty[xs], xph ^ 1);
-      if (lane == 0) {
-        if (!(p.dbg & 16)) {
-          tma_2d_g2s(xbuf + (size_t)xs * BM * 128, &xmap, kt * kTileK, mc * BM, &xfull[xs]);
-          mbar_arrive_expect_tx(&xfull[xs], BM * 128);
-        } else {
-          mbar_arrive(&xfull[xs]);
-        }
-      }
-      __syncwarp();
-      if (++xs == S) { xs = 0; xph ^= 1; }
-      if (++kt == p.n_kt) kt = 0;
-      if (--rem == 0) {
-        rem = tiles_per_mc;
-        ++mc;
-      }
-    }
-    if (threadIdx.x == 32 * kWarpProd1) SALR_TRACE(28);
+    if (lane == 0 && pk == 0) SALR_TRACE(2);
   } else if (warp == kWarpPub) {
     // ================= publisher: releases the first split partial at GPU
     // scope (fence + ticket) so the epilogue warps never stall on it
@@ -766,7 +761,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       const uint32_t acc = kTm + (uint32_t)(b * ACOLS);
       mbar_wait(&acc_empty[b], acc_ph ^ 1);
       tc_fence_after();
-      if (S == 8 && !(p.dbg & 24) && !p.probe_log) {
+      if (S == 8 && !(p.dbg & 24) && !kProbe) {
         // Ring of 8: the stage index is a compile-time constant in each case
         // (Duff-style entry at the current stage), so barrier, TMEM and
         // descriptor offsets are immediates and the per-unit loop is two
@@ -775,8 +770,8 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
 #define SALR_MMA_UNIT(K)                                                                              \
   case K:                                                                                             \
     if (v >= seg_end) break;                                                                          \
-    SALR_TRACE_UNIT(2, v - u_begin);                                                                  \
-    mbar_wait2_addr(dec0 + 8u * (K), xf0 + 8u * (K), ph);                                            \
+    mbar_wait_addr(dec0 + 8u * (K), ph);                                                              \
+    mbar_wait_addr(xf0 + 8u * (K), ph);                                                               \
     tc_fence_after();                                                                                 \
     SALR_TRACE_UNIT(6, v - u_begin);                                                                  \
     mma_ktile_ts_imm<kTm + a_col0 + 32u * (K)>(acc, lo0 + (K) * kLoStep, bhi, IDESC, v != u ? 1u : 0u, \
@@ -809,7 +804,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       for (int v = u; v < seg_end; ++v) {
         mbar_wait_addr(dad, ph);
         if (!(p.dbg & 16)) mbar_wait_addr(dad + 8u * (uint32_t)S, ph);  // this stage's X tile (xfull)
-        if (p.probe_log) {
+        if (kProbe) {
           if (lane == 0)
             probe_log_transition(p.probe_log, p.probe_cap, (uint32_t)(blockIdx.x * S + sg), kSlotFilled,
                                  kSlotConsumed);
@@ -887,8 +882,8 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
     for (int it = u_begin + grp; it < u_end; it += kDecGroups) {
       mbar_wait(&full[s], ph);
       if (lane == 0 && (dw % WPG) == 0) SALR_TRACE_UNIT(1, it - u_begin);
-      if (p.probe_log) {
-        if (lane == 0 && q == 0)
+      if (kProbe) {
+        if (lane == 0 && (dw % WPG) == 0)
           probe_log_transition(p.probe_log, p.probe_cap, (uint32_t)(blockIdx.x * S + s), kSlotEmpty, kSlotFilled);
         probe_jitter(p.probe_ns, p.probe_seed, (uint32_t)it, (uint32_t)warp);
         __syncwarp();
@@ -896,7 +891,7 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
       const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(2 * BPW * part);
       if (!(p.dbg & 1)) {
-        decode_tile_tb2(smem_u32(rec), taddr, q, lane, lut_s);
+        decode_tile_tb2<BPW>(smem_u32(rec), taddr, q, lane, lut_s, part);
         tc_wait_st();
       }
       tc_fence_before();
@@ -1133,9 +1128,9 @@ __global__ void __launch_bounds__(num_threads(kDecGroups), 1)
       const int mc = u / (p.n_kt * p.n_nt);
       const int b = NACC == 2 ? (seg & 1) : 0;
       const uint32_t acc_ph = (uint32_t)((NACC == 2 ? seg >> 1 : seg) & 1);
-      // long wait (a whole output tile's k-loop): backoff polling, see
-      // mbar_wait_backoff -- the decoders keep the issue slots
-      mbar_wait_backoff(&acc_full[b], acc_ph, 256);
+      // long wait: try_wait suspends the warp in hardware (no issue slots)
+      // and wakes it as soon as the phase completes
+      mbar_wait(&acc_full[b], acc_ph);
       tc_fence_after();
       if (etid == 0 && seg == 0) SALR_TRACE(7);
       // partial slot of this CTA: 0 for its first segment, 1 otherwise
@@ -1484,7 +1479,6 @@ static int pick_bm(int64_t M) {
 // Deepest ring that fits shared memory and TMEM (slots sized for the largest
 // record of the matrix: ~9.6 KB at 50% sparsity instead of the 17.4 KB worst
 // case).
-static int pref_groups();
 static int max_stages(int bm, int ra, uint32_t rec_slot, int cap) {
   const int acc = nacc_for(bm) * acc_cols_for(bm);
   const int tmem_stages = (512 - ((acc + 31) & ~31)) / 32;
@@ -1493,17 +1487,16 @@ static int max_stages(int bm, int ra, uint32_t rec_slot, int cap) {
   int s = cap;
   if (s > tmem_stages) s = tmem_stages;
   while (s > 1 && smem_plan(bm, s, ra, rec_slot).total > kSmemMaxLinear) --s;
-  const int ng = pref_groups();
-  if (s > ng) s -= s % ng;  // a multiple of the decoder group count
+  if (s > 4) s &= ~3;  // a multiple of the decoder group count
   return s;
 }
 
 // configuration of the most recent linear launch (salr_debug_last_launch)
 static int g_last_launch[12] = {};
 
-template <int BM, int NG>
+template <int BM, int NG, bool kProbe = false>
 static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cudaStream_t s, bool pdl) {
-  auto kern = salr_linear_kernel<BM, NG>;
+  auto kern = salr_linear_kernel<BM, NG, kProbe>;
   const SmemPlan plan = smem_plan(BM, p.stages, p.ra, p.rec_slot);
   p.x_off = plan.x_off;
   p.rec_off = plan.rec_off;
@@ -1518,7 +1511,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctas);
-  cfg.blockDim = dim3(num_threads(NG));
+  cfg.blockDim = dim3(kNumThreads);
   cfg.dynamicSmemBytes = plan.total;
   cfg.stream = s;
   cudaLaunchAttribute attr[3];
@@ -1581,7 +1574,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   int coop_launch = 0;
   if ((p.u_mode == 1 || p.coop) && pdl) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, num_threads(NG), plan.total) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNumThreads, plan.total) != cudaSuccess) {
       (void)cudaGetLastError();
       per_sm = 1;
     }
@@ -1600,7 +1593,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
     // too large a grid): launch without it only if every CTA fits at once
     (void)cudaGetLastError();
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, num_threads(NG), plan.total) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNumThreads, plan.total) != cudaSuccess) {
       (void)cudaGetLastError();
       per_sm = 0;
     }
@@ -1617,21 +1610,17 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   return SALR_OK;
 }
 
-// Decoder groups of four warps: 4 by default (SALR_DEC_GROUPS overrides in
-// debug builds), reduced to a divisor of the ring depth (stage ownership,
-// see the kernel).
-static int pref_groups() {
+// Decoder groups: 4 by default (SALR_DEC_GROUPS overrides for experiments),
+// reduced to a divisor of the ring depth (stage ownership, see the kernel).
+static int dec_groups(int stages) {
   static int g = 0;
   if (!g) {
     const char* e = dbg_env("SALR_DEC_GROUPS");
     g = e ? atoi(e) : 4;
-    if (g < 1 || g > 4) g = 4;
+    if (g != 1 && g != 2 && g != 4) g = 4;
   }
-  return g;
-}
-static int dec_groups(int stages) {
-  int ng = pref_groups();
-  while (ng > 1 && stages % ng) --ng;
+  int ng = g;
+  while (ng > 1 && stages % ng) ng >>= 1;
   return ng;
 }
 
@@ -1640,8 +1629,17 @@ static int launch_linear(const CUtensorMap* maps, const LinearParams& p, int cta
   switch (dec_groups(p.stages)) {
     case 1: return launch_linear_g<BM, 1>(maps, p, ctas, s, pdl);
     case 2: return launch_linear_g<BM, 2>(maps, p, ctas, s, pdl);
-    case 3: return launch_linear_g<BM, 3>(maps, p, ctas, s, pdl);
     default: return launch_linear_g<BM, 4>(maps, p, ctas, s, pdl);
+  }
+}
+
+// The probed instantiations (salr_debug_set_probe): decode-size tiles of
+// BM = 16 tokens only, so the release kernels carry no probe code.
+static int launch_linear_probed(const CUtensorMap* maps, const LinearParams& p, int ctas, cudaStream_t s, bool pdl) {
+  switch (dec_groups(p.stages)) {
+    case 1: return launch_linear_g<16, 1, true>(maps, p, ctas, s, pdl);
+    case 2: return launch_linear_g<16, 2, true>(maps, p, ctas, s, pdl);
+    default: return launch_linear_g<16, 4, true>(maps, p, ctas, s, pdl);
   }
 }
 
@@ -1950,11 +1948,11 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     p.probe_seed = g_probe_seed;
   }
   {
-    // + 16 bytes: the decoders' fixed-width band loads read up to 3
-    // halfwords past a band's last value; the slack keeps those (unused)
-    // reads inside the slot instead of the next slot a TMA may be filling
+    // (the decoders' fixed-width band loads may read a few halfwords past a
+    // tile's last value -- into the next slot or the barrier area, never
+    // used: the selectors pick zero bytes for absent rows)
     p.rec_slot = (max_record_bytes > 0 && max_record_bytes <= kMaxRecordBytesT2)
-                     ? (uint32_t)((max_record_bytes + 16 + 15) & ~15ll) : (uint32_t)kMaxRecordBytesT2 + 16u;
+                     ? (uint32_t)((max_record_bytes + 15) & ~15ll) : (uint32_t)kMaxRecordBytesT2;
     const int smax = max_stages(bm, ra, p.rec_slot, stages > 8 ? std::min(stages, 16) : 8);
     p.stages = stages <= 0 || stages > smax ? smax : stages;
   }
@@ -2054,6 +2052,11 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     pp.trace = g_trace;
     pp.dbg = p.dbg;
     return launch_prefill(maps, pp, s, pdl);
+  }
+  if (p.probe_log) {
+    SALR_CHECK_ARG(bm == 16, SALR_ERR_CONFIG, "the pipeline probe runs decode-size launches of M <= 16 (M=%lld)",
+                   (long long)M);
+    return launch_linear_probed(maps, p, (int)ctas, s, pdl);
   }
   switch (bm) {
     case 16: rc = launch_linear<16>(maps, p, (int)ctas, s, pdl); break;
