@@ -12,8 +12,10 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 # full capture of the bench's dominant launch (gate|up, M=32), gate at M=32/1 and the prefill kernel
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:salr_linear_kernel -s 2 -c 1 \
   -o gpurun_out/prof_gateup32 python tools/profile_linear.py --shape gateup --tokens 32 --reps 4 > gpurun_out/ncu_fullgu.log 2>&1
+if [ -n "$PREFILL_NCU" ]; then
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:salr_prefill_kernel -s 1 -c 1 \
   -o gpurun_out/prof_prefill_gate2048 python tools/profile_linear.py --shape gate --tokens 2048 --reps 3 > gpurun_out/ncu_fullpf.log 2>&1
+fi
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:salr_linear_kernel -s 2 -c 1 \
   -o gpurun_out/prof_gate32 python tools/profile_linear.py --shape gate --tokens 32 --reps 4 > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:salr_linear_kernel -s 2 -c 1 \

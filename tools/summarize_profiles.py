@@ -84,7 +84,12 @@ def main(tag):
                "share_by_kernel": share, "launches": ll},
               open(os.path.join(PROF, f"{tag}_launch_list.json"), "w"), indent=1)
 
-    summ = {}
+    # keep earlier captures this run did not redo (e.g. the prefill kernel)
+    try:
+        summ = {k: v for k, v in json.load(open(os.path.join(PROF, "ncu_summary.json"))).items()
+                if isinstance(v, dict)}
+    except Exception:
+        summ = {}
     logs = {"prof_gateup32": "ncu_fullgu.log", "prof_gate32": "ncu_full.log", "prof_gate1": "ncu_full1.log",
             "prof_prefill_gate2048": "ncu_fullpf.log"}
     for name, shape, tokens in (("prof_gateup32", "gateup", 32), ("prof_gate32", "gate", 32),
