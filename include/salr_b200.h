@@ -119,6 +119,18 @@ int salr_tb_from_tb2_count(const uint8_t* records2, const uint32_t* tile_off2, i
 int salr_tb_from_tb2_write(const uint8_t* records2, const uint32_t* tile_off2, int64_t rows, int64_t cols,
                           const uint32_t* tile_off, uint8_t* records, void* stream);
 
+/* ---- NM24 compute format (2:4 along the columns; csrc/salr_format.cuh) -- */
+/* For matrices under the reference's 2:4 mask (prune.py:238-248: at most 2
+ * nonzeros in every group of 4 consecutive columns of a row).  Fixed 9216
+ * bytes per 64x128 tile (n_tiles = n_nt * n_kt, n-tile-major), no offset
+ * table.  Write: from a dense bf16 matrix (leading dim ld); groups with more
+ * than 2 nonzeros are added to *bad_groups (device u32, zeroed by the caller)
+ * and the records are then not a valid encoding.  Decode: dense bf16. */
+int salr_nm24_write(const void* dense_bf16, int64_t rows, int64_t cols, int64_t ld, uint8_t* records,
+                    uint32_t* bad_groups, void* stream);
+int salr_nm24_decode(const uint8_t* records, int64_t rows, int64_t cols, void* dense_bf16, int64_t ld,
+                     void* stream);
+
 /* ---- exact magnitude-prune masks (reference prune.py:213-255) ----------- */
 /* Global methods: mask[i] = 1 for exactly `keep` entries -- the largest
  * scores (non-negative, float32 dtype 0 or float64 dtype 2), ties broken
@@ -196,6 +208,9 @@ int salr_debug_set_probe(void* log, size_t log_words, int max_delay_ns, uint32_t
  * range |U| < 2^37).  The Python layer sets it when the bound
  * K * max|X| * max|A_cat| falls outside [2^-6, 2^34]. */
 #define SALR_FLAG_U_FP32 2
+/* flags: SALR_FLAG_NM24: records are NM24 (salr_nm24_write); tile_off and
+ * max_record_bytes are ignored.  Decode-size kernel at every M. */
+#define SALR_FLAG_NM24 4
 int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const uint8_t* records,
                         const uint32_t* tile_off, int64_t max_record_bytes, int64_t N, const void* acat, const void* bcat_t,
                         int64_t r_pad, void* y, int y_dtype, int64_t ldy, void* workspace,

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsalr_b200.so")
 SOURCES = ["salr_codec.cu", "salr_linear.cu", "salr_prune.cu"]
-HEADERS = ["salr_format.cuh", "salr_ptx.cuh", "salr_status.cuh"]
+HEADERS = ["salr_format.cuh", "salr_ptx.cuh", "salr_status.cuh", "salr_prefill.cuh", "salr_chain.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -28,6 +28,7 @@ __all__ = ["DTYPE_F32", "popcount8", "build_lut", "bytes_per_row", "BitmapSparse
            "encode", "decode", "decode_block", "write_container", "read_container",
            "header_bytes", "container_size_bytes", "compression_ratio", "kept_count"]
 
+NM24_RECORD_BYTES = 9216  # fixed NM24 tile record (csrc/salr_format.cuh)
 DTYPE_F32 = 0  # the only stored precision of the container format (bitmap.py:48)
 
 _MAGIC = b"SALR"
@@ -119,6 +120,7 @@ class BitmapSparseMatrix:
         self.n_kt, self.n_nt, self.n_tiles = _lib.geometry(self.rows, self.cols)
         self._byte_starts = None
         self._tb2 = None
+        self._nm24 = None  # NM24 records (2:4 matrices, use_nm24())
 
     @classmethod
     def _wrap(cls, rows, cols, value_dtype, records, tile_off):
@@ -179,6 +181,9 @@ class BitmapSparseMatrix:
         transient, not cached)."""
         if self.records is not None:
             return self.records, self.tile_off
+        if self._tb2 is None:  # NM24 only: dense bf16 -> TB
+            e = encode(self._nm24_dense(), "bf16")
+            return e.records, e.tile_off
         rec2, off2, _ = self._tb2
         lib = _lib.load()
         st = _lib.stream_ptr()
@@ -228,6 +233,8 @@ class BitmapSparseMatrix:
     def max_record_bytes(self) -> int:
         """Largest TB record (bytes); sizes the linear kernel's ring slots."""
         if getattr(self, "_max_rec", None) is None:
+            if self.tile_off is None:
+                return self._tb2[2] if self._tb2 is not None else NM24_RECORD_BYTES
             off = self.tile_off.to(torch.int64) & 0xFFFFFFFF
             self._max_rec = int(16 * (off[1:] - off[:-1]).max().item()) if off.numel() > 1 else 0
         return self._max_rec
@@ -242,6 +249,8 @@ class BitmapSparseMatrix:
             n += int(self.records.numel()) + 4 * int(self.tile_off.numel())
         if self._tb2 is not None:
             n += int(self._tb2[0].numel()) + 4 * int(self._tb2[1].numel())
+        if self._nm24 is not None:
+            n += int(self._nm24.numel())
         if self._byte_starts is not None:
             n += 8 * int(self._byte_starts.numel())
         return n
@@ -264,13 +273,14 @@ class BitmapSparseMatrix:
             sb = self.to_bf16()
             lib = _lib.load()
             st = _lib.stream_ptr()
-            off2 = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=sb.records.device)
-            _lib.check(lib.salr_tb2_count(_lib.ptr(sb.records), _u32(sb.tile_off), self.rows, self.cols,
-                                          _u32(off2), st))
+            rec, toff = sb.tb()
+            off2 = torch.empty(self.n_tiles + 1, dtype=torch.int32, device=rec.device)
+            _lib.check(lib.salr_tb2_count(_lib.ptr(rec), _u32(toff), self.rows, self.cols, _u32(off2), st))
             units = int(off2[-1].item()) & 0xFFFFFFFF
-            rec2 = torch.empty(16 * units, dtype=torch.uint8, device=sb.records.device)
-            _lib.check(lib.salr_tb2_write(_lib.ptr(sb.records), _u32(sb.tile_off), self.rows, self.cols,
-                                          _u32(off2), _lib.ptr(rec2), st))
+            rec2 = torch.empty(16 * units, dtype=torch.uint8, device=rec.device)
+            _lib.check(lib.salr_tb2_write(_lib.ptr(rec), _u32(toff), self.rows, self.cols, _u32(off2),
+                                          _lib.ptr(rec2), st))
+            del rec, toff
             o = off2.to(torch.int64) & 0xFFFFFFFF
             mx = int(16 * (o[1:] - o[:-1]).max().item()) if o.numel() > 1 else 0
             self._tb2 = (rec2, off2, mx)
@@ -278,6 +288,55 @@ class BitmapSparseMatrix:
             if self.value_dtype == "bf16":
                 self.records = self.tile_off = None  # TB2 is the one resident format
         return self._tb2
+
+    # ------------------------------------------------------------------ NM24 (2:4)
+    def is_nm24(self) -> bool:
+        """True when NM24 is this matrix's compute format (``use_nm24``)."""
+        return self._nm24 is not None
+
+    def use_nm24(self) -> "BitmapSparseMatrix":
+        """Make NM24 the compute format: for a matrix under the reference's
+        2:4 mask (``prune.py:238-248``, at most 2 nonzeros in every group of
+        4 consecutive columns of a row) the linear kernel then reads fixed
+        9216-byte tiles (1.125 B/weight) and expands them with byte permutes
+        instead of the bitmap decoder -- same dense tile, bit-identical
+        results.  Raises FormatError (matrix unchanged) when some group holds
+        more than 2 nonzeros.  A bf16 matrix then keeps only NM24 resident
+        (``tb()`` / ``compute_format()`` rebuild the others on request);
+        float32 values are rounded to bf16 as for TB2 and the TB records stay.
+        Built once on the current stream, never inside a graph capture."""
+        if self._nm24 is not None:
+            return self
+        if torch.cuda.is_current_stream_capturing():
+            raise SalrError("build the compute format (use_nm24()) before capturing a CUDA graph")
+        dense = _decode_window(self, 0, self.rows, 0, self.cols, torch.bfloat16)
+        lib = _lib.load()
+        rec = torch.empty(self.n_tiles * NM24_RECORD_BYTES, dtype=torch.uint8, device=dense.device)
+        bad = torch.zeros(1, dtype=torch.int32, device=dense.device)
+        _lib.check(lib.salr_nm24_write(_lib.ptr(dense), self.rows, self.cols, self.cols, _lib.ptr(rec),
+                                       _lib.ptr(bad), _lib.stream_ptr()))
+        nbad = int(bad.item())
+        if nbad:
+            raise FormatError(f"{nbad} groups of 4 columns hold more than 2 nonzeros: the matrix is not 2:4")
+        self._nm24 = rec
+        if self.value_dtype == "bf16":
+            self.records = self.tile_off = None
+            self._tb2 = None
+        return self
+
+    def _nm24_dense(self) -> torch.Tensor:
+        out = torch.empty((self.rows, self.cols), dtype=torch.bfloat16, device=self._nm24.device)
+        _lib.check(_lib.load().salr_nm24_decode(_lib.ptr(self._nm24), self.rows, self.cols, _lib.ptr(out),
+                                                self.cols, _lib.stream_ptr()))
+        return out
+
+    def kernel_operand(self):
+        """(records, tile_off, max_record_bytes, nm24) the linear kernel reads:
+        NM24 when ``use_nm24`` made it the compute format, else TB2."""
+        if self._nm24 is not None:
+            return self._nm24, None, NM24_RECORD_BYTES, True
+        rec2, off2, mx = self.compute_format()
+        return rec2, off2, mx, False
 
     @classmethod
     def from_compute_format(cls, rows: int, cols: int, records2: torch.Tensor, tile_off2: torch.Tensor):
@@ -327,8 +386,12 @@ class BitmapSparseMatrix:
             r2, o2 = cut(self._tb2[0], self._tb2[1])
             oo = o2.to(torch.int64)
             obj._tb2 = (r2, o2, int(16 * (oo[1:] - oo[:-1]).max()) if oo.numel() > 1 else 0)
+        if self._nm24 is not None:  # fixed-size tiles: a plain byte range
+            obj._nm24 = self._nm24[t0 * NM24_RECORD_BYTES:t1 * NM24_RECORD_BYTES].clone()
         obj._max_rec = None
-        if obj.records is not None:
+        if obj.records is None and obj._tb2 is None:
+            obj.nnz = int((obj._nm24_dense() != 0).sum())
+        elif obj.records is not None:
             obj.max_record_bytes  # computed eagerly (never inside a graph capture)
             obj.nnz = _tile_nnz_sum(obj.records, obj.tile_off.to(torch.int64)[:-1])
         else:
@@ -345,7 +408,10 @@ class BitmapSparseMatrix:
 
     @property
     def device(self) -> torch.device:
-        return (self.records if self.records is not None else self._tb2[0]).device
+        for t in (self.records, self._tb2[0] if self._tb2 is not None else None, self._nm24):
+            if t is not None:
+                return t.device
+        raise SalrError("matrix holds no records")
 
     def __repr__(self):
         return (f"BitmapSparseMatrix(rows={self.rows}, cols={self.cols}, nnz={self.nnz}, "

@@ -494,6 +494,72 @@ __global__ void tb_from_tb2_kernel(const uint8_t* __restrict__ records2, const u
   }
 }
 
+// ------------------------------------------------------------------ NM24
+// NM24 records (salr_format.cuh) from a dense bf16 matrix: grid = n_tiles,
+// block = 512, thread (band b, 4-column group g).  Groups with more than 2
+// nonzeros are counted in *bad (the matrix is not 2:4 along its columns).
+// Nonzero = not +-0, as the reference encoder (bitmap.py:150-165).
+__global__ void __launch_bounds__(512) nm24_write_kernel(const uint16_t* __restrict__ dense, int64_t rows,
+                                                         int64_t cols, int64_t ld, int64_t n_kt,
+                                                         uint8_t* __restrict__ out, uint32_t* bad) {
+  const int64_t t = blockIdx.x;
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const int b = threadIdx.x >> 5, g = threadIdx.x & 31;
+  const int64_t c0 = nt * kTileN + 4 * g;
+  uint32_t w[4];
+  uint32_t masks = 0, over = 0;
+  for (int r = 0; r < 4; ++r) {
+    const int64_t row = kt * kTileK + 4 * b + r;
+    uint32_t m = 0, v0 = 0, v1 = 0, n = 0;
+    for (int c = 0; c < 4; ++c) {
+      const uint32_t bits = (row < rows && c0 + c < cols) ? dense[row * ld + c0 + c] : 0u;
+      if (bits & 0x7FFFu) {
+        m |= 1u << c;
+        if (n == 0) v0 = bits;
+        else if (n == 1) v1 = bits;
+        ++n;
+      }
+    }
+    over += n > 2;
+    w[r] = v0 | v1 << 16;
+    masks |= m << (4 * r);
+  }
+  uint8_t* rec = out + (size_t)t * kNmRecBytes;
+  *reinterpret_cast<uint4*>(rec + 16 * (32 * b + g)) = make_uint4(w[0], w[1], w[2], w[3]);
+  *reinterpret_cast<uint16_t*>(rec + kNmValBytes + 16 * (32 * (b >> 3) + g) + 4 * ((b & 7) >> 1) + 2 * (b & 1)) =
+      (uint16_t)masks;
+  if (over) atomicAdd(bad, over);
+}
+
+// Dense bf16 matrix (ld) from NM24 records; same thread mapping.
+__global__ void __launch_bounds__(512) nm24_decode_kernel(const uint8_t* __restrict__ records, int64_t rows,
+                                                          int64_t cols, int64_t n_kt, uint16_t* __restrict__ dense,
+                                                          int64_t ld) {
+  const int64_t t = blockIdx.x;
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const int b = threadIdx.x >> 5, g = threadIdx.x & 31;
+  const int64_t c0 = nt * kTileN + 4 * g;
+  const uint8_t* rec = records + (size_t)t * kNmRecBytes;
+  const uint4 wv = *reinterpret_cast<const uint4*>(rec + 16 * (32 * b + g));
+  const uint32_t w[4] = {wv.x, wv.y, wv.z, wv.w};
+  const uint32_t masks = *reinterpret_cast<const uint16_t*>(rec + kNmValBytes + 16 * (32 * (b >> 3) + g) +
+                                                             4 * ((b & 7) >> 1) + 2 * (b & 1));
+  for (int r = 0; r < 4; ++r) {
+    const int64_t row = kt * kTileK + 4 * b + r;
+    if (row >= rows) break;
+    const uint32_t m = (masks >> (4 * r)) & 0xFu;
+    uint32_t n = 0;
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v = 0;
+      if ((m >> c) & 1u) {
+        v = n == 0 ? (w[r] & 0xFFFFu) : n == 1 ? (w[r] >> 16) : 0u;
+        ++n;
+      }
+      if (c0 + c < cols) dense[row * ld + c0 + c] = (uint16_t)v;
+    }
+  }
+}
+
 extern "C" {
 
 int salr_version(void) { return 1; }
@@ -673,6 +739,32 @@ int salr_tb_from_tb2_write(const uint8_t* records2, const uint32_t* tile_off2, i
   geometry(rows, cols, &n_kt, &n_nt);
   tb_from_tb2_kernel<<<(unsigned)(n_kt * n_nt), 128, 0, static_cast<cudaStream_t>(stream)>>>(records2, tile_off2,
                                                                                              tile_off, records);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_nm24_write(const void* dense_bf16, int64_t rows, int64_t cols, int64_t ld, uint8_t* records,
+                    uint32_t* bad_groups, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(ld >= cols, SALR_ERR_SHAPE, "ld < cols");
+  SALR_CHECK_ARG(dense_bf16 && records && bad_groups, SALR_ERR_CONFIG, "null pointer");
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  nm24_write_kernel<<<(unsigned)(n_kt * n_nt), 512, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint16_t*>(dense_bf16), rows, cols, ld, n_kt, records, bad_groups);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_nm24_decode(const uint8_t* records, int64_t rows, int64_t cols, void* dense_bf16, int64_t ld,
+                     void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(ld >= cols, SALR_ERR_SHAPE, "ld < cols");
+  SALR_CHECK_ARG(dense_bf16 && records, SALR_ERR_CONFIG, "null pointer");
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  nm24_decode_kernel<<<(unsigned)(n_kt * n_nt), 512, 0, static_cast<cudaStream_t>(stream)>>>(
+      records, rows, cols, n_kt, static_cast<uint16_t*>(dense_bf16), ld);
   SALR_LAUNCH_CHECK();
   return SALR_OK;
 }

@@ -28,6 +28,21 @@ constexpr int kT2Mask = 144;
 constexpr int kT2Val = 1168;
 constexpr int kMaxRecordBytesT2 = kT2Val + kTileK * kTileN * 2;  // 17552
 
+// NM24: compute format of a matrix whose nonzeros are 2:4 along the columns
+// (at most 2 in every group of 4 consecutive columns of a row -- the
+// reference's N:M mask, prune.py:238-248).  Fixed 9216 bytes per 64x128 tile,
+// n-tile-major like TB2 (no offset table: tile t starts at 9216 * t):
+//   values  [16 bands][32 groups] x 16 B: for the 4 rows of the band one u32
+//           each, v0 | v1 << 16 = the group's first and second nonzero (bf16;
+//           0 when absent), at 16 * (32 * band + group)
+//   masks   [2 halves][32 groups] x 16 B at 8192: u32 word w of (half h,
+//           group g) holds rows 32h + 8w .. +7, row i's 4-bit column mask
+//           (bit j = column 4g + j nonzero) at bits 4i .. 4i+3
+// 1.125 B/weight; a decoder lane selects its column's value of each row with
+// byte permutes -- no prefix sums, no variable offsets.
+constexpr int kNmValBytes = 8192;
+constexpr int kNmRecBytes = 9216;
+
 enum : int { kF32 = 0, kBF16 = 1, kF64 = 2 };
 
 __host__ __device__ inline int value_bytes(int dtype) { return dtype == kF32 ? 4 : 2; }

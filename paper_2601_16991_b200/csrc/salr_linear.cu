@@ -7,19 +7,21 @@
 // B200 design:
 //   * swap-AB: the tensor core computes a Y^T tile = W^T tile (128 output
 //     columns = M_mma 128) x X^T (N_mma = BM tokens), fp32 accumulator in TMEM.
-//   * warp roles of one persistent CTA per SM (25 warps):
-//       warps 0, 24 TMA producers (even / odd work units): each TB2 record
+//   * warp roles of one persistent CTA per SM (24 warps, 6 per sub-partition):
+//       warps 0, 3  TMA producers (even / odd work units): each TB2 / NM24 record
 //                   (1-D bulk copy, L2 evict-first) into a ring of up to 8
 //                   shared-memory stages (full/empty mbarriers, expect_tx),
 //                   the X tile (2-D tensor map, 128B swizzle) on its own
 //                   barrier; records of the first ring go out before the
 //                   programmatic-launch wait.
 //       warp 1      MMA issuer (one elected lane), TMEM allocator.
-//       warp 2      publisher: releases the CTA's first split-K partial.
+//       warp 2      publisher: releases the CTA's first split-K partial;
+//                   fills the decoders' nibble table at entry.
 //       warps 4-19  decoders, four groups of four warps.  Group g decodes
 //                   units = g (mod 4); warp (g, q) owns output columns
 //                   32q..32q+31 == TMEM lanes 32q..32q+31, expands the 64
 //                   rows of its column from the band runs of the TB2 record
+//                   (or selects them from the NM24 record of a 2:4 matrix)
 //                   and writes bf16 pairs along K with tcgen05.st straight
 //                   into the TMEM A operand of the next MMA -- decoded tiles
 //                   never touch shared memory.
@@ -75,6 +77,7 @@ struct LinearParams {
   int cluster;        // > 1: every output tile is split over exactly the `cluster`
                       // CTAs of one thread-block cluster; reduced through DSMEM
   uint32_t rec_slot;  // bytes per ring slot: the largest record of this matrix, 16-aligned
+  int nm24;           // 1: records are NM24 (fixed kNmRecBytes per tile, tile_off unused)
   int dbg;            // timing experiments only: 1 = skip decode, 2 = skip record loads
   unsigned long long* trace;  // optional per-CTA event timestamps (globaltimer ns), [G][32]
   // Pipeline probe (salr_debug_set_probe; null = off): device form of the
@@ -103,7 +106,14 @@ constexpr int kUSlice = 64;  // K rows per dynamically claimed U slice
 constexpr int kDoneTicketOff = 16 * 1024;  // second counter per split tile (workspace ticket area)
 constexpr int kUAccElems = 256 * 128;  // per parity buffer: M <= 256 rows x r_pad <= 128
 constexpr int kNumDecWarps = 16;
-constexpr int kNumThreads = 800;               // 25 warps
+// The odd-unit producer runs on warp 3 (sub-partition 3, otherwise idle):
+// with it on a 25th warp, sub-partition 0 hosted both producers next to four
+// decoder warps and an epilogue warp, and its decoders lagged the group by
+// ~1 us per tile (unit traces); measured 3-7 % faster per launch.
+#ifndef SALR_PROD1_WARP
+#define SALR_PROD1_WARP 3
+#endif
+constexpr int kNumThreads = SALR_PROD1_WARP == 3 ? 768 : 800;  // 24 / 25 warps
 constexpr int kFirstDecWarp = 4;
 constexpr int kFirstEpiWarp = 20;
 // warp layout helpers of the chained-linear kernel (salr_chain.cuh): NG
@@ -307,9 +317,56 @@ __device__ __forceinline__ void decode_tile_tb2(uint32_t rec_s, uint32_t taddr, 
   }
 }
 
+// NM24 tile decoder (salr_format.cuh), same TMEM result as decode_tile_tb2.
+// Lane = output column 32q + lane = column j of 4-column group g.  Per 8 rows
+// one mask word gives, as bit 7 of byte p, "row 2p (<<4) / 2p+1 kept in
+// column j" and "a lower column of the group is kept too" (then this column
+// holds the group's second value v1): sign-replicating permutes turn those
+// bits into the byte mask and the value selector of the row pair.
+template <int BPW = 16>
+__device__ __forceinline__ void decode_tile_nm24(uint32_t rec_s, uint32_t taddr, int q, uint32_t lane, int part = 0) {
+  const uint32_t g = 8u * (uint32_t)q + (lane >> 2), j = lane & 3u;
+  const uint32_t lower = 0x11111111u * ((1u << j) - 1u);  // columns below j, every nibble
+  const uint32_t sh = 3u - j;
+#pragma unroll
+  for (int pp = 0; pp < 16 / BPW; ++pp) {
+    if (pp != part) continue;
+#pragma unroll
+    for (int c4 = 0; c4 < BPW / 4; ++c4) {
+      const int b0 = BPW * pp + 4 * c4;  // bands b0..b0+3 = rows 4*b0 .. 4*b0+15
+      const uint2 mw = lds_v2_u32(rec_s + kNmValBytes + 16u * (32u * (uint32_t)(b0 >> 3) + g) +
+                                  4u * (uint32_t)((b0 >> 1) & 3));
+      uint32_t packed[8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // mask word h: bands b0 + 2h, b0 + 2h + 1
+        const uint32_t m = h ? mw.y : mw.x;
+        const uint32_t kx = (m << sh) & 0x88888888u;                     // kept, bit 4i+3
+        const uint32_t bx = ((m & lower) + 0x77777777u) & 0x88888888u;  // second value
+        const uint32_t klo = kx << 4, blo = bx << 4;
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) {
+          const uint4 w = lds_v4_u32(rec_s + 16u * (32u * (uint32_t)(b0 + 2 * h + bb) + g));
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            const uint32_t pidx = 2u * bb + t;  // row pair within the mask word
+            // byte mask of the pair (16-bit halves) and the value selector
+            // (nibble pairs: +2 picks v1's bytes)
+            const uint32_t sel = (0x8u | pidx) * 0x11u | ((0xCu | pidx) * 0x11u) << 8;
+            const uint32_t vsel = (0x8u | pidx) | (0xCu | pidx) << 4;
+            const uint32_t msk = prmt(klo, kx, sel);
+            const uint32_t vs = (prmt(blo, bx, vsel) & 0x2222u) | 0x5410u;
+            packed[4 * h + 2 * bb + t] = prmt(t ? w.z : w.x, t ? w.w : w.y, vs) & msk;
+          }
+        }
+      }
+      SALR_TMEM_ST_X8(taddr + 8u * c4, packed);
+    }
+  }
+}
+
 // kDecGroups decoder groups (group g decodes units it = g mod kDecGroups).
-constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPub = 2;  // warp 3 idle
-constexpr int kWarpProd1 = 24;
+constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPub = 2;
+constexpr int kWarpProd1 = SALR_PROD1_WARP;
 
 template <int BM, int kDecGroups, bool kProbe = false>
 __global__ void __launch_bounds__(kNumThreads, 1)
@@ -388,8 +445,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     o0 = o1 = 0u;
     if (v < u_end) {
       const int t = v % tiles_per_mc;
-      o0 = __ldg(p.tile_off + t);
-      o1 = __ldg(p.tile_off + t + 1);
+      if (p.nm24) {
+        o0 = (uint32_t)t * (kNmRecBytes / 16);
+        o1 = o0 + kNmRecBytes / 16;
+      } else {
+        o0 = __ldg(p.tile_off + t);
+        o1 = __ldg(p.tile_off + t + 1);
+      }
     }
   };
   // X tile of unit v into stage st (the input; may have to wait for the
@@ -510,7 +572,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   // nibble table of the decoders: static shared memory, so its address is a
   // compile-time constant folded into the decoders' loads
   __shared__ __align__(128) uint64_t s_lut[16];
-  if (warp == 3 && lane < 16) s_lut[lane] = nib_lut_entry(lane);
+  if (warp == (kWarpProd1 == 3 ? kWarpPub : 3) && lane < 16) s_lut[lane] = nib_lut_entry(lane);
   const uint32_t lut_s = smem_u32(s_lut);
   if (warp == kWarpMma) {
     tmem_alloc(tmem_slot, 512);
@@ -891,7 +953,10 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const uint8_t* rec = recbuf + (size_t)s * p.rec_slot;
       const uint32_t taddr = tmem + lane_tm + a_col0 + 32u * s + (uint32_t)(2 * BPW * part);
       if (!(p.dbg & 1)) {
-        decode_tile_tb2<BPW>(smem_u32(rec), taddr, q, lane, lut_s, part);
+        if (p.nm24)
+          decode_tile_nm24<BPW>(smem_u32(rec), taddr, q, lane, part);
+        else
+          decode_tile_tb2<BPW>(smem_u32(rec), taddr, q, lane, lut_s, part);
         tc_wait_st();
       }
       tc_fence_before();
@@ -1905,6 +1970,8 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   SALR_CHECK_ARG((reinterpret_cast<uintptr_t>(x) & 15) == 0, SALR_ERR_SHAPE, "x must be 16-byte aligned");
   SALR_CHECK_ARG(r_pad == 0 || r_pad == 64 || r_pad == 128, SALR_ERR_CONFIG, "r_pad must be 0, 64 or 128");
   SALR_CHECK_ARG(r_pad == 0 || (acat && bcat_t), SALR_ERR_CONFIG, "adapters need acat and bcat_t");
+  const bool nm24 = (flags & SALR_FLAG_NM24) != 0;
+  SALR_CHECK_ARG(records && (nm24 || tile_off), SALR_ERR_CONFIG, "records / tile_off missing");
   SALR_CHECK_ARG(y_dtype == kF32 || y_dtype == kBF16, SALR_ERR_DOMAIN, "y dtype must be f32 or bf16");
   SALR_CHECK_ARG(ldy >= N, SALR_ERR_SHAPE, "ldy < N");
   SALR_CHECK_ARG(workspace_bytes >= salr_linear_workspace_bytes(M, N, K, r_pad, num_ctas), SALR_ERR_CONFIG,
@@ -1951,8 +2018,10 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     // (the decoders' fixed-width band loads may read a few halfwords past a
     // tile's last value -- into the next slot or the barrier area, never
     // used: the selectors pick zero bytes for absent rows)
-    p.rec_slot = (max_record_bytes > 0 && max_record_bytes <= kMaxRecordBytesT2)
+    p.rec_slot = nm24 ? (uint32_t)kNmRecBytes
+                 : (max_record_bytes > 0 && max_record_bytes <= kMaxRecordBytesT2)
                      ? (uint32_t)((max_record_bytes + 15) & ~15ll) : (uint32_t)kMaxRecordBytesT2;
+    p.nm24 = nm24 ? 1 : 0;
     const int smax = max_stages(bm, ra, p.rec_slot, stages > 8 ? std::min(stages, 16) : 8);
     p.stages = stages <= 0 || stages > smax ? smax : stages;
   }
@@ -2033,7 +2102,9 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   const int64_t pf_items = ((M + 128 * kPfMG - 1) / (128 * kPfMG)) * p.n_nt;
   // The prefill kernel has no split-K: it needs enough (512-token x
   // 128-column) items to occupy the GPU (measured crossover ~3/4 of the SMs).
-  if (M > kPrefillMinM && num_ctas <= 0 && !no_prefill && 4 * pf_items >= 3 * (int64_t)sm_count()) {
+  // (NM24 matrices always take the decode-size kernel: it covers any M in
+  // m-chunks; the prefill kernel reads TB2 only)
+  if (M > kPrefillMinM && num_ctas <= 0 && !no_prefill && !nm24 && 4 * pf_items >= 3 * (int64_t)sm_count()) {
     // prefill-size M: decode each weight tile once per 512 tokens
     PrefillParams pp = {};
     pp.records = records;

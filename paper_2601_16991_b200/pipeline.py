@@ -178,7 +178,7 @@ def _prep_x(x, K: int, check_finite: bool):
 # the in-kernel U accumulator (int64 fixed point, 2^-26) is exact enough for
 # |U| bounds inside this window; outside it U comes from the fp32 pre-kernel
 _U_FIXED_MIN, _U_FIXED_MAX = 2.0 ** -6, 2.0 ** 34
-_FLAG_PDL, _FLAG_U_FP32 = 1, 2
+_FLAG_PDL, _FLAG_U_FP32, _FLAG_NM24 = 1, 2, 4
 
 _launches = 0
 
@@ -209,7 +209,7 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     _lib.require_cuda()
     if not isinstance(s, BitmapSparseMatrix):
         raise SalrError("s must be a BitmapSparseMatrix")
-    rec2, off2, max_rec2 = s.compute_format()
+    rec2, off2, max_rec2, nm24 = s.kernel_operand()
     xb, xmax = _prep_x(x, s.rows, check_finite)
     M = int(xb.shape[0])
     N = s.cols
@@ -227,7 +227,7 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
         # two fp32 device GEMMs after the launch (rare; the fused path covers
         # the paper's configurations, R = 32..128)
         fused, tail = fused.split(128)
-    flags = _FLAG_PDL if pdl else 0
+    flags = (_FLAG_PDL if pdl else 0) | (_FLAG_NM24 if nm24 else 0)
     if fused is not None:
         acat, bct = fused.device_operands()
         r_pad = fused.r_pad
@@ -301,6 +301,8 @@ def salr_chain(x, linears, outs, *, pdl: bool = False, workspace: torch.Tensor |
             raise ShapeError("chained linears need K a multiple of 8")
         if fused is not None and fused.total_rank > 128:
             raise ConfigError("chained linears take fused rank <= 128")
+        if s.is_nm24():
+            raise ConfigError("chained linears read TB2 records; NM24 matrices run through salr_linear")
         rec2, off2, mx = s.compute_format()
         acat = bct = None
         r_pad = 0
