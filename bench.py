@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--batches", default="1,8,32", help="extra decode batch sizes reported per-M")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cublas", action="store_true")
+    ap.add_argument("--no-nm24", action="store_true", help="skip the 2:4 (NM24) stack leg")
     ap.add_argument("--chain", action="store_true",
                     help="one persistent launch per layer (salr_chain) instead of one launch per linear")
     return ap.parse_args()
@@ -328,14 +329,18 @@ def _prune_threshold(sparsity):
     return 0.02 * q  # |w| quantile of N(0, 0.02^2): magnitude pruning at `sparsity`
 
 
-def gen_layer(layer, world, rank, sparsity, device):
+def gen_layer(layer, world, rank, sparsity, device, pattern="magnitude"):
     """Dense inputs of one stack layer, seeded per (layer, rank) so any layer
     can be regenerated alone: {fused name: (W_hat bf16 (k x n_local),
     [(A, B, scale)] bf16-exact fp32 adapter factors, (k, n_local), (c0, c1))}.
-    The reference arm regenerates layer 0 with the same seeds."""
+    The reference arm regenerates layer 0 with the same seeds.  pattern
+    "2:4": the reference's N:M mask (prune.py:238-248, 2 largest |w| of every
+    4 consecutive columns) instead of global magnitude pruning."""
     import torch
+    import paper_2601_16991_b200 as S
     g = torch.Generator(device=device).manual_seed(1234 + 7919 * layer + 17 * rank)
     thr = _prune_threshold(sparsity)
+    nm = S.PruneConfig(0.5, S.PruneMethod.SEMI_STRUCTURED_NM, nm=(2, 4))
     out = {}
     for name in STACK_ORDER:
         k, parts = FUSED[name]
@@ -343,7 +348,10 @@ def gen_layer(layer, world, rank, sparsity, device):
         c0, c1 = shard_cols(n, world, rank)
         nl = c1 - c0
         w = (torch.randn(k, nl, generator=g, device=device) * 0.02).to(torch.bfloat16)
-        w = torch.where(w.float().abs() < thr, torch.zeros_like(w), w)
+        if pattern == "2:4":
+            w = S.prune(w.float(), nm).to(torch.bfloat16)
+        else:
+            w = torch.where(w.float().abs() < thr, torch.zeros_like(w), w)
         ads = []
         p0 = 0
         for _, pw in parts:  # LoRA r16 + residual r16 per original linear, on its own columns
@@ -365,16 +373,19 @@ def gen_x(tokens, device):
     return torch.randn(tokens, 4096, generator=g, device=device).bfloat16()
 
 
-def build_stack(layers, world, rank, sparsity, device):
+def build_stack(layers, world, rank, sparsity, device, pattern="magnitude"):
     """Per layer: {fused name: (BitmapSparseMatrix shard, FusedAdapters shard, (k, n_local), col range)}."""
     import paper_2601_16991_b200 as S
 
     stack = []
     for layer in range(layers):
         lin = {}
-        for name, (w, ads, kn, cols) in gen_layer(layer, world, rank, sparsity, device).items():
+        for name, (w, ads, kn, cols) in gen_layer(layer, world, rank, sparsity, device, pattern).items():
             s = S.encode(w, value_dtype="bf16")
-            s.compute_format()  # the linear kernel's operand format, built once at load
+            if pattern == "2:4":
+                s.use_nm24()  # fixed-size 2:4 tiles: the compute format of this stack
+            else:
+                s.compute_format()  # the linear kernel's operand format, built once at load
             del w
             fused = S.fuse([S.AdapterPair(a, b, 16, sc) for a, b, sc in ads])
             fused.device_operands()
@@ -519,6 +530,55 @@ def cublas_times(stack, tokens, reps=20):
     return res
 
 
+def nm24_leg(args, dev, local, cublas):
+    """The paper's published configuration (2:4 semi-structured, PAPER.md
+    Table inference): the same 32-layer stack with weights under the
+    reference's 2:4 mask, held in the NM24 compute format.  Stack tokens/s per
+    decode batch, per-linear kernel times at --tokens, roofline of the fused
+    kernel on its own record bytes, layer-0 check.  cuBLAS dense bf16 times do
+    not depend on the weight values: the main leg's are reused."""
+    import torch
+    M = args.tokens
+    stack = build_stack(args.layers, 1, 0, 0.5, dev, pattern="2:4")
+    torch.cuda.synchronize()
+    per_m = {}
+    for mb in [int(v) for v in args.batches.split(",") if v]:
+        r = make_runner(stack, mb, 1, 0)
+        r.x_in.copy_(gen_x(mb, dev))
+        r.step(r.x_in)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            r.step(r.x_in)
+        n = max(5, args.steps // 2)
+        ms, clk = time_steps(g.replay, n, 3, 1, local)
+        per_m[str(mb)] = {"tokens_per_s": mb / (ms / n / 1e3), "ms_per_step": ms / n, "clocks": clk}
+        del g, r
+    per = per_linear_kernel_times(stack, M)
+    rec_bytes = sum(stack[0][n][0].device_bytes for n in per)  # the 9216-byte tiles each launch streams
+    k_us = sum(v["us"] for v in per.values())
+    alg = sum(v["compressed_bytes"] for v in per.values())
+    hbm_peak = peaks()[0]
+    out = {
+        "format": "NM24 (fixed 9216-byte 64x128 tiles: 2 bf16 + a 4-bit column mask per row group of 4)",
+        "mask": "reference N:M rule, n=2 m=4 along the columns (prune.py:238-248), device mask",
+        "per_batch": per_m,
+        "per_linear": per,
+        "kernel_us_per_layer": k_us,
+        "roofline": {"bound": "hbm", "achieved_record_bytes": rec_bytes / (k_us * 1e-6) / 1e9,
+                     "achieved_algorithmic": alg / (k_us * 1e-6) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": rec_bytes / (k_us * 1e-6) / 1e9 / hbm_peak},
+        "resident_bytes_per_weight": sum(lin[n][0].device_bytes for lin in stack for n in STACK_ORDER)
+        / sum(lin[n][2][0] * lin[n][2][1] for lin in stack for n in STACK_ORDER),
+        "check": layer_check(stack[0], gen_x(M, dev), gen_layer(0, 1, 0, 0.5, dev, "2:4")),
+    }
+    if cublas is not None:
+        out["cublas_dense_bf16_speedup"] = cublas["us_per_layer"] / k_us
+    del stack
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_salr(args):
     import torch
     import torch.distributed as dist
@@ -624,6 +684,8 @@ def run_salr(args):
             cb_us = sum(v["us"] for v in cb.values())
             extra["cublas_dense_bf16"] = {"us_per_layer": cb_us, "salr_us_per_layer": k_us,
                                           "speedup": cb_us / k_us, "per_linear": cb}
+        if world == 1 and not args.no_nm24:
+            extra["two_four"] = None  # filled after the main per-batch runs (own stack)
         per_m = {}
         if world == 1:
             for mb in [int(v) for v in args.batches.split(",") if v]:
@@ -650,6 +712,8 @@ def run_salr(args):
                   "resident_bytes_per_weight": resident / (dense_bf16 / 2),
                   "format": "TB2 records + tile offsets only (the compute format; TB rebuilt on demand)"}
         check = layer_check(stack[0], x0, gen_layer(0, world, rank, args.sparsity, dev))
+        if "two_four" in extra:
+            extra["two_four"] = nm24_leg(args, dev, local, extra.get("cublas_dense_bf16"))
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             c = cpu_sample(M, args.sparsity)

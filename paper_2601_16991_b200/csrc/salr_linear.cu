@@ -109,11 +109,20 @@ constexpr int kNumDecWarps = 16;
 // The odd-unit producer runs on warp 3 (sub-partition 3, otherwise idle):
 // with it on a 25th warp, sub-partition 0 hosted both producers next to four
 // decoder warps and an epilogue warp, and its decoders lagged the group by
-// ~1 us per tile (unit traces); measured 3-7 % faster per launch.
+// ~1 us per tile (unit traces).  The block size only sets the register
+// budget then: 24 warps (80 registers) for BM = 16 tiles, 25 (72 registers,
+// warp 24 idle) for larger ones -- measured best per tile size on the
+// 32-layer stack (A/B, tools/gpu_ab_bench.sh).
 #ifndef SALR_PROD1_WARP
 #define SALR_PROD1_WARP 3
 #endif
-constexpr int kNumThreads = SALR_PROD1_WARP == 3 ? 768 : 800;  // 24 / 25 warps
+__host__ __device__ constexpr int threads_for(int bm) {
+#ifdef SALR_NUM_WARPS
+  return 32 * SALR_NUM_WARPS + 0 * bm;
+#else
+  return (SALR_PROD1_WARP == 3 && bm == 16) ? 768 : 800;
+#endif
+}
 constexpr int kFirstDecWarp = 4;
 constexpr int kFirstEpiWarp = 20;
 // warp layout helpers of the chained-linear kernel (salr_chain.cuh): NG
@@ -369,7 +378,7 @@ constexpr int kWarpProd0 = 0, kWarpMma = 1, kWarpPub = 2;
 constexpr int kWarpProd1 = SALR_PROD1_WARP;
 
 template <int BM, int kDecGroups, bool kProbe = false>
-__global__ void __launch_bounds__(kNumThreads, 1)
+__global__ void __launch_bounds__(threads_for(BM), 1)
     salr_linear_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap bmap,
                        const __grid_constant__ CUtensorMap uhimap, const __grid_constant__ CUtensorMap ulomap,
                        const LinearParams p) {
@@ -1356,7 +1365,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     const int ng = (rows + 3) / 4;
     const int g0 = rank * ng / np, g1 = (rank + 1) * ng / np;
     const uint32_t sp = smem_u32(xbuf);
-    for (int e = threadIdx.x; e < (g1 - g0) * kTileN; e += kNumThreads) {
+    for (int e = threadIdx.x; e < (g1 - g0) * kTileN; e += threads_for(BM)) {
       const int nl = e % kTileN, m = 4 * (g0 + e / kTileN);
       const uint32_t a = sp + (uint32_t)((nl * (BM + 4) + m) * 4);
       // every remote load in flight before the (rank-ordered) sums
@@ -1576,7 +1585,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctas);
-  cfg.blockDim = dim3(kNumThreads);
+  cfg.blockDim = dim3(threads_for(BM));
   cfg.dynamicSmemBytes = plan.total;
   cfg.stream = s;
   cudaLaunchAttribute attr[3];
@@ -1639,7 +1648,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
   int coop_launch = 0;
   if ((p.u_mode == 1 || p.coop) && pdl) {
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNumThreads, plan.total) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads_for(BM), plan.total) != cudaSuccess) {
       (void)cudaGetLastError();
       per_sm = 1;
     }
@@ -1658,7 +1667,7 @@ static int launch_linear_g(const CUtensorMap* maps, LinearParams p, int ctas, cu
     // too large a grid): launch without it only if every CTA fits at once
     (void)cudaGetLastError();
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kNumThreads, plan.total) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads_for(BM), plan.total) != cudaSuccess) {
       (void)cudaGetLastError();
       per_sm = 0;
     }
