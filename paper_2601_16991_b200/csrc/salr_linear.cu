@@ -465,11 +465,18 @@ __global__ void __launch_bounds__(threads_for(BM), 1)
   };
   // X tile of unit v into stage st (the input; may have to wait for the
   // preceding kernel under programmatic dependent launch)
+  // The X tile lands on the stage's `decoded` barrier (one producer arrival
+  // + its bytes next to the decoder warps' arrivals), so the MMA issuer --
+  // the CTA's serial path -- waits on one barrier per unit.
   auto issue_x = [&](int v, int st) {
+    if (p.dbg & 16) {  // experiment: no X tiles
+      mbar_arrive(&decoded[st]);
+      return;
+    }
     const int kt = v % p.n_kt;
     const int mc = v / tiles_per_mc;
-    tma_2d_g2s(xbuf + (size_t)st * BM * 128, &xmap, kt * kTileK, mc * BM, &xfull[st]);
-    mbar_arrive_expect_tx(&xfull[st], BM * 128);
+    tma_2d_g2s(xbuf + (size_t)st * BM * 128, &xmap, kt * kTileK, mc * BM, &decoded[st]);
+    mbar_arrive_expect_tx(&decoded[st], BM * 128);
   };
   // Issue unit pv.  The copies go out before arrive.expect_tx (the phase
   // cannot complete before the arrive, and issuing the copy first keeps it
@@ -496,7 +503,7 @@ __global__ void __launch_bounds__(threads_for(BM), 1)
       const uint32_t bytes = (p.dbg & 2) ? 0u : (o1 - o0) * 16u;
       if (bytes) bulk_g2s_hint(recbuf + (size_t)ps * p.rec_slot, p.records + (size_t)o0 * 16u, bytes, &full[ps], pol_stream);
       mbar_arrive_expect_tx(&full[ps], bytes);
-      if (with_x && !(p.dbg & 16)) issue_x(pv, ps);
+      if (with_x) issue_x(pv, ps);
       SALR_TRACE_UNIT(0, pv - u_begin);
     }
     __syncwarp();
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(threads_for(BM), 1)
         mbar_init(&full[s], 1);
         mbar_init(&xfull[s], 1);
         mbar_init(&empty[s], 1);
-        mbar_init(&decoded[s], WPG);
+        mbar_init(&decoded[s], WPG + 1);  // decoder warps + the X tile's producer
       }
       for (int b = 0; b < 2; ++b) {
         mbar_init(&acc_full[b], 1);
@@ -739,8 +746,7 @@ __global__ void __launch_bounds__(threads_for(BM), 1)
     if (lane == 0 && producer) {
       const int first_seg_end = min(u_end, u_begin - u_begin % p.n_kt + p.n_kt);
       const int pre = min(first_seg_end, u_begin + S);
-      if (!(p.dbg & 16))
-        for (int v = u_begin + pk; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
+      for (int v = u_begin + pk; v < pre; v += NP) issue_x(v, (v - u_begin) % S);
     }
     __syncwarp();
     if (threadIdx.x == 0) SALR_TRACE(28);
@@ -820,7 +826,6 @@ __global__ void __launch_bounds__(threads_for(BM), 1)
     // uniform registers.
     constexpr uint32_t kTm = 0u;
     const uint32_t atm0 = kTm + a_col0, dec0 = smem_u32(decoded), emp0 = smem_u32(empty);
-    const uint32_t xf0 = smem_u32(xfull);
     int s = 0, seg = 0;
     uint32_t ph = 0, ad_ph = 0;
     int u = u_begin;
@@ -842,7 +847,6 @@ __global__ void __launch_bounds__(threads_for(BM), 1)
   case K:                                                                                             \
     if (v >= seg_end) break;                                                                          \
     mbar_wait_addr(dec0 + 8u * (K), ph);                                                              \
-    mbar_wait_addr(xf0 + 8u * (K), ph);                                                               \
     tc_fence_after();                                                                                 \
     SALR_TRACE_UNIT(6, v - u_begin);                                                                  \
     mma_ktile_ts_imm<kTm + a_col0 + 32u * (K)>(acc, lo0 + (K) * kLoStep, bhi, IDESC, v != u ? 1u : 0u, \
@@ -873,8 +877,7 @@ __global__ void __launch_bounds__(threads_for(BM), 1)
       uint32_t lo = lo0 + (uint32_t)sg * kLoStep, atm = atm0 + 32u * (uint32_t)sg;
       uint32_t dad = dec0 + 8u * (uint32_t)sg, ead = emp0 + 8u * (uint32_t)sg;
       for (int v = u; v < seg_end; ++v) {
-        mbar_wait_addr(dad, ph);
-        if (!(p.dbg & 16)) mbar_wait_addr(dad + 8u * (uint32_t)S, ph);  // this stage's X tile (xfull)
+        mbar_wait_addr(dad, ph);  // decoded tile and X tile
         if (kProbe) {
           if (lane == 0)
             probe_log_transition(p.probe_log, p.probe_cap, (uint32_t)(blockIdx.x * S + sg), kSlotFilled,
