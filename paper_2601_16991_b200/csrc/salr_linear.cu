@@ -1693,7 +1693,10 @@ static int dec_groups(int stages) {
   static int g = 0;
   if (!g) {
     const char* e = dbg_env("SALR_DEC_GROUPS");
-    g = e ? atoi(e) : 4;
+#ifndef SALR_DEFAULT_DEC_GROUPS
+#define SALR_DEFAULT_DEC_GROUPS 4
+#endif
+    g = e ? atoi(e) : SALR_DEFAULT_DEC_GROUPS;
     if (g != 1 && g != 2 && g != 4) g = 4;
   }
   int ng = g;
