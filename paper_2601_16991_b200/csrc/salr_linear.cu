@@ -969,7 +969,9 @@ __global__ void __launch_bounds__(threads_for(BM), 1)
           decode_tile_nm24<BPW>(smem_u32(rec), taddr, q, lane, part);
         else
           decode_tile_tb2<BPW>(smem_u32(rec), taddr, q, lane, lut_s, part);
+        if (lane == 0 && (dw % WPG) == 0) SALR_TRACE_UNIT(11, it - u_begin);
         tc_wait_st();
+        if (lane == 0 && (dw % WPG) == 0) SALR_TRACE_UNIT(13, it - u_begin);
       }
       tc_fence_before();
       __syncwarp();

@@ -18,8 +18,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:salr
 fi
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:salr_linear_kernel -s 2 -c 1 \
   -o gpurun_out/prof_gate32 python tools/profile_linear.py --shape gate --tokens 32 --reps 4 > gpurun_out/ncu_full.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:salr_linear_kernel -s 2 -c 1 \
-  -o gpurun_out/prof_gate1 python tools/profile_linear.py --shape gate --tokens 1 --reps 4 > gpurun_out/ncu_full1.log 2>&1
-timeout 900 python tools/sweep.py --tokens 1,8,32,2048 > gpurun_out/sweep.jsonl 2> gpurun_out/sweep.err
-timeout 600 python tools/bench_linear.py --tokens 128,2048 --shapes q,gate,down --cublas --pdl > gpurun_out/bl_prefill.jsonl 2>&1
+timeout 300 python tools/nm24_perf.py > gpurun_out/nm24_perf.jsonl 2>&1
 echo done

@@ -77,6 +77,10 @@ print("stage life-cycle averages (us):")
 print(f"  issue -> full seen by decoders : {avg([r[1] - r[0] for r in rows if r[1] and r[0]]):.3f}")
 print(f"  decode (full -> last warp done): {avg([r[4] - r[1] for r in rows if r[4] and r[1]]):.3f}")
 print(f"  decoded -> MMA ready           : {avg([r[6] - r[4] for r in rows if r[6] and r[4]]):.3f}")
+ex = {e: [(us(dd[e, i]) if int(dd[e, i]) else None) for i in range(len(rows))] for e in (11, 13)}
+print(f"  warp q0: full -> decode issued : {avg([ex[11][i] - rows[i][1] for i in range(len(rows)) if ex[11][i] and rows[i][1]]):.3f}")
+print(f"  warp q0: tcgen05.wait::st      : {avg([ex[13][i] - ex[11][i] for i in range(len(rows)) if ex[13][i] and ex[11][i]]):.3f}")
+print(f"  warp q0: stores done -> arrive : {avg([rows[i][3] - ex[13][i] for i in range(len(rows)) if ex[13][i] and rows[i][3]]):.3f}")
 print(f"  MMA ready -> issued            : {avg([r[5] - r[6] for r in rows if r[5] and r[6]]):.3f}")
 for S2 in (8, 4):
     print(f"  MMA issued -> issue of unit+{S2}   : {avg([rows[i + S2][0] - rows[i][5] for i in range(n - S2) if rows[i][5]]):.3f}")
