@@ -43,16 +43,26 @@ def f(v):
 
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
-    b = last_json_line(os.path.join(OUT, "bench.json"))
-    json.dump(b, open(os.path.join(PROF, f"{tag}_bench_stack.json"), "w"), indent=1)
-    r = last_json_line(os.path.join(OUT, "bench_ref.json"))
-    json.dump(r, open(os.path.join(PROF, f"{tag}_bench_reference_arm.json"), "w"), indent=1)
+    # (a second call may carry only some of the outputs: each part is
+    # processed when its file is present)
+    if os.path.exists(os.path.join(OUT, "bench.json")):
+        b = last_json_line(os.path.join(OUT, "bench.json"))
+        json.dump(b, open(os.path.join(PROF, f"{tag}_bench_stack.json"), "w"), indent=1)
+    if os.path.exists(os.path.join(OUT, "bench_ref.json")):
+        r = last_json_line(os.path.join(OUT, "bench_ref.json"))
+        json.dump(r, open(os.path.join(PROF, f"{tag}_bench_reference_arm.json"), "w"), indent=1)
     for src, dst in (("bl_all.jsonl", "per_linear_decode.jsonl"), ("bl_prefill.jsonl", "per_linear_prefill.jsonl"),
-                     ("sweep.jsonl", "sweep_4096x14336.jsonl")):
+                     ("sweep.jsonl", "sweep_4096x14336.jsonl"), ("nm24_perf.jsonl", "nm24_per_linear.jsonl")):
         p = os.path.join(OUT, src)
         if os.path.exists(p):
             shutil.copy(p, os.path.join(PROF, f"{tag}_{dst}"))
 
+    if os.path.exists(os.path.join(OUT, "launches.csv")):
+        launch_list(tag)
+    ncu_summaries(tag)
+
+
+def launch_list(tag):
     # launch list: per-launch duration and DRAM bytes of our kernels
     rows = list(csv.reader(open(os.path.join(OUT, "launches.csv"))))
     hdr = next(i for i, row in enumerate(rows) if "Metric Name" in row)
@@ -84,6 +94,9 @@ def main(tag):
                "share_by_kernel": share, "launches": ll},
               open(os.path.join(PROF, f"{tag}_launch_list.json"), "w"), indent=1)
 
+
+
+def ncu_summaries(tag):
     # keep earlier captures this run did not redo (e.g. the prefill kernel)
     try:
         summ = {k: v for k, v in json.load(open(os.path.join(PROF, "ncu_summary.json"))).items()
@@ -91,9 +104,10 @@ def main(tag):
     except Exception:
         summ = {}
     logs = {"prof_gateup32": "ncu_fullgu.log", "prof_gate32": "ncu_full.log", "prof_gate1": "ncu_full1.log",
-            "prof_prefill_gate2048": "ncu_fullpf.log"}
+            "prof_prefill_gate2048": "ncu_fullpf.log", "prof_nm24_gate32": "ncu_fullnm.log"}
     for name, shape, tokens in (("prof_gateup32", "gateup", 32), ("prof_gate32", "gate", 32),
-                                ("prof_gate1", "gate", 1), ("prof_prefill_gate2048", "gate", 2048)):
+                                ("prof_gate1", "gate", 1), ("prof_prefill_gate2048", "gate", 2048),
+                                ("prof_nm24_gate32", "gate", 32)):
         alg = ALG[shape]
         try:  # the profiled script prints the matrix's algorithmic bytes
             for line in open(os.path.join(OUT, logs[name])):
