@@ -158,8 +158,22 @@ def _workspace(M: int, N: int, K: int, r_pad: int, num_ctas: int, device) -> tor
 
 
 def _prep_x(x, K: int, check_finite: bool):
-    """bf16, K padded to a multiple of 8; with ``check_finite`` also max|X|
-    (one reduction: a non-finite entry makes it non-finite) -> DomainError."""
+    """(X, max|X| or None, leading dimension): bf16, K padded to a multiple of
+    8; with ``check_finite`` also max|X| (one reduction: a non-finite entry
+    makes it non-finite) -> DomainError.  A bf16 device matrix whose rows are
+    16-byte aligned -- e.g. the leading columns of the previous linear's
+    output -- is passed as it is with its row stride (no copy kernel between
+    two chained launches)."""
+    if (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16 and x.dim() == 2
+            and x.shape[0] >= 1 and x.shape[1] == K and K % 8 == 0 and x.stride(1) == 1
+            and x.stride(0) >= K and x.stride(0) % 8 == 0 and x.data_ptr() % 16 == 0
+            and x.device.index == torch.cuda.current_device()):
+        xmax = None
+        if check_finite:
+            xmax = float(x.abs().amax())
+            if not math.isfinite(xmax):
+                raise DomainError("x contains non-finite entries")
+        return x, xmax, int(x.stride(0))
     xm = as_matrix(x, "x", require_finite=False)
     if xm.shape[1] != K:
         raise ShapeError(f"x cols {xm.shape[1]} != sparse rows {K}")
@@ -172,7 +186,10 @@ def _prep_x(x, K: int, check_finite: bool):
         xm = xm.to(torch.bfloat16)
     if K % 8:
         xm = torch.nn.functional.pad(xm, (0, 8 - K % 8))
-    return xm.contiguous(), xmax
+    xm = xm.contiguous()
+    if xm.data_ptr() % 16:  # e.g. a single-row slice at an odd column offset
+        xm = xm.clone()
+    return xm, xmax, int(xm.shape[1])
 
 
 # the in-kernel U accumulator (int64 fixed point, 2^-26) is exact enough for
@@ -210,7 +227,7 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     if not isinstance(s, BitmapSparseMatrix):
         raise SalrError("s must be a BitmapSparseMatrix")
     rec2, off2, max_rec2, nm24 = s.kernel_operand()
-    xb, xmax = _prep_x(x, s.rows, check_finite)
+    xb, xmax, ldx = _prep_x(x, s.rows, check_finite)
     M = int(xb.shape[0])
     N = s.cols
     if fused is not None and (fused.d_in != s.rows or fused.d_out != s.cols):
@@ -245,7 +262,7 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     global _launches
     _launches += 1 if (fused is None or (M <= 256 and not flags & _FLAG_U_FP32)) else 2
     _lib.check(_lib.load().salr_linear_forward(
-        _lib.ptr(xb), M, s.rows, int(xb.shape[1]), _lib.ptr(rec2), _lib.ptr(off2), max_rec2, N,
+        _lib.ptr(xb), M, s.rows, ldx, _lib.ptr(rec2), _lib.ptr(off2), max_rec2, N,
         _lib.ptr(acat), _lib.ptr(bct), r_pad, _lib.ptr(out), _lib.dtype_code(out.dtype), N,
         _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), flags, _lib.stream_ptr()))
     if tail is not None:
@@ -283,7 +300,7 @@ def salr_chain(x, linears, outs, *, pdl: bool = False, workspace: torch.Tensor |
     L = len(linears)
     if not 1 <= L <= 4 or len(outs) != L:
         raise ConfigError("a chain holds 1..4 linears and one output per linear")
-    xb, _ = _prep_x(x, linears[0][0].rows, False)
+    xb, _, ldx0 = _prep_x(x, linears[0][0].rows, False)
     M = int(xb.shape[0])
     if M > 256:
         raise ConfigError("chained linears are decode-size (M <= 256)")
@@ -316,7 +333,7 @@ def salr_chain(x, linears, outs, *, pdl: bool = False, workspace: torch.Tensor |
     ws = workspace if workspace is not None else _chain_workspace(M, L, xb.device)
     global _launches
     _launches += 1
-    _lib.check(_lib.load().salr_chain_forward(ctypes.addressof(arr), L, _lib.ptr(xb), M, int(xb.shape[1]),
+    _lib.check(_lib.load().salr_chain_forward(ctypes.addressof(arr), L, _lib.ptr(xb), M, ldx0,
                                               _lib.ptr(ws), int(ws.numel()), _FLAG_PDL if pdl else 0,
                                               _lib.stream_ptr()))
     return outs
@@ -399,7 +416,7 @@ def bench(x_shape, s: BitmapSparseMatrix, cfg: PipelineConfig, repeats: int = 5,
     b = pipelined_matmul(x, s, over)
     if not torch.equal(a, b):
         raise VerificationError("serial and overlapped outputs differ")
-    xd, _ = _prep_x(x, s.rows, True)
+    xd, _, _ = _prep_x(x, s.rows, True)
 
     def timed(c):
         pipelined_matmul(xd, s, c)

@@ -273,3 +273,32 @@ def test_pdl_chain_matches_serial(S, M):
         torch.cuda.synchronize()
         for i in range(12):
             assert torch.equal(ref[i], outs[i]), i
+
+
+@pytest.mark.parametrize("M", [1, 8, 32, 100])
+@pytest.mark.parametrize("adapters", [True, False])
+def test_strided_input_no_copy(S, M, adapters):
+    """The leading columns of a wider bf16 output (the stack's o / down
+    inputs) go to the kernel as they are, with their row stride: same result
+    as the contiguous copy, in-kernel U included, and no copy kernel."""
+    g = torch.Generator().manual_seed(77 + M)
+    K, N, W = 1024, 768, 1536
+    w = (torch.randn(K, N, generator=g) * 0.03).bfloat16().float()
+    w[torch.rand(K, N, generator=g) < 0.5] = 0
+    s = S.encode(w.cuda(), value_dtype="bf16")
+    s.compute_format()
+    f = None
+    if adapters:
+        f = S.fuse([S.AdapterPair((torch.randn(K, 16, generator=g) / 32).bfloat16().float(),
+                                  (torch.randn(16, N, generator=g) * 0.03).bfloat16().float(), 16)])
+    wide = torch.randn(M, W, generator=g).bfloat16().cuda()
+    view = wide[:, 256:256 + K]  # 512-byte offset: rows stay 16-byte aligned
+    from paper_2601_16991_b200.pipeline import _prep_x
+    xb, _, ldx = _prep_x(view, K, False)
+    assert xb.data_ptr() == view.data_ptr() and ldx == W
+    for dt in (torch.float32, torch.bfloat16):
+        assert torch.equal(S.salr_linear(view, s, f, out_dtype=dt), S.salr_linear(view.contiguous(), s, f, out_dtype=dt))
+    # unaligned or non-bf16 views still work through the copy
+    odd = wide[:, 3:3 + K]
+    assert _prep_x(odd, K, False)[0].data_ptr() != odd.data_ptr()
+    assert torch.equal(S.salr_linear(odd, s, f), S.salr_linear(odd.contiguous(), s, f))
