@@ -167,13 +167,14 @@ def _last_launch():
     return dict(zip(keys, list(info)))
 
 
-@pytest.mark.parametrize("M", [16, 32, 100])
+@pytest.mark.parametrize("M", [8, 16, 32, 100])
 @pytest.mark.parametrize("adapters", [False, True])
 def test_split_k_reduction_modes(S, M, adapters):
     """The three split-K reductions give the same answer: DSMEM within a
     thread-block cluster (tiles split over exactly np CTAs of one cluster),
     cooperative global, last-CTA global.  K=4096 (64 k-tiles) x 4096 columns:
-    128 CTAs x 16 units -> clusters of 4."""
+    128 CTAs x 16 units -> clusters of 4 where the cooperative reduction is
+    off (M < 16)."""
     g = torch.Generator().manual_seed(77 + M)
     K, N = 4096, 4096
     w = (torch.randn(K, N, generator=g) * 0.02).bfloat16().float()
@@ -197,7 +198,9 @@ def test_split_k_reduction_modes(S, M, adapters):
         assert_close(y.cpu().numpy(), ref, f"M={M} ctas={ctas} {info}")
         y2 = S.salr_linear(x, s, fused, num_ctas=ctas)
         assert torch.equal(y, y2)  # run-to-run determinism of every mode
-    assert 0 in seen and max(seen) >= 2, seen
+    assert 0 in seen, seen
+    if M < 16:
+        assert max(seen) >= 2, seen
 
 
 @pytest.mark.parametrize("rank", [16, 64])
