@@ -2070,10 +2070,15 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     // K dimension exactly: every split output tile is then shared by
     // CTAs that finish together, so the split-K reduction does not wait on
     // a straggler (q/o/k/v/down at M >= 16, where the reduction is heavy).
+    // Also accepted: a grid that is a multiple of the output-tile count --
+    // every tile then split over exactly c / tiles CTAs, whose contiguous
+    // unit ranges never straddle a tile boundary (q|k|v at M=32: 144 CTAs
+    // for 48 tiles, 2.3 us faster than 148).
+    const int64_t tiles = p.units / p.n_kt;
     for (int64_t c = ctas; c >= (6 * ctas + 6) / 7; --c) {
-      if (p.units % c) continue;
       const int64_t per = p.units / c;
-      if (p.n_kt % per == 0 || per % p.n_kt == 0) {
+      const bool even = p.units % c == 0 && (p.n_kt % per == 0 || per % p.n_kt == 0);
+      if (even || c % tiles == 0) {
         ctas = c;
         break;
       }

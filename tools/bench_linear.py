@@ -58,7 +58,7 @@ def graph_time(fn, reps):
 
 
 for name in a.shapes.split(","):
-    K, N = synthetic.LLAMA3_8B_LINEARS[name]
+    K, N = dict(synthetic.LLAMA3_8B_LINEARS, qkv=(4096, 6144), gateup=(4096, 28672))[name]
     mats, fus, dense = [], [], []
     for c in range(a.copies):
         w = (torch.randn(K, N, generator=g, device="cuda") * 0.02).bfloat16()
