@@ -2065,7 +2065,12 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   // fixup for a pipeline that never fills.
   constexpr int64_t kMinUnitsPerCta = 6;
   int64_t ctas = num_ctas > 0 ? num_ctas : std::min<int64_t>(sm_count(), (p.units + kMinUnitsPerCta - 1) / kMinUnitsPerCta);
-  if (num_ctas <= 0 && M >= 16 && !(dbg_env("SALR_NO_ALIGNED_GRID"))) {
+// (not for a single token: there the split-K fixup is one row and the
+// extra SMs win -- down at M=1 is 2 us slower on 128 CTAs than on 148)
+#ifndef SALR_ALIGNED_GRID_MIN_M
+#define SALR_ALIGNED_GRID_MIN_M 2
+#endif
+  if (num_ctas <= 0 && M >= SALR_ALIGNED_GRID_MIN_M && !(dbg_env("SALR_NO_ALIGNED_GRID"))) {
     // Prefer a grid (>= 6/7 of the SMs) whose per-CTA unit ranges tile the
     // K dimension exactly: every split output tile is then shared by
     // CTAs that finish together, so the split-K reduction does not wait on
