@@ -278,7 +278,7 @@ def test_pdl_chain_matches_serial(S, M):
             assert torch.equal(ref[i], outs[i]), i
 
 
-@pytest.mark.parametrize("M", [1, 8, 32, 100])
+@pytest.mark.parametrize("M", [1, 8, 32, 100, 300])
 @pytest.mark.parametrize("adapters", [True, False])
 def test_strided_input_no_copy(S, M, adapters):
     """The leading columns of a wider bf16 output (the stack's o / down
@@ -305,3 +305,22 @@ def test_strided_input_no_copy(S, M, adapters):
     odd = wide[:, 3:3 + K]
     assert _prep_x(odd, K, False)[0].data_ptr() != odd.data_ptr()
     assert torch.equal(S.salr_linear(odd, s, f), S.salr_linear(odd.contiguous(), s, f))
+
+
+def test_strided_input_prefill(S):
+    """A strided bf16 view through the prefill kernel (M=2048): same result
+    as its contiguous copy (the X tensor map carries the row stride)."""
+    g = torch.Generator().manual_seed(5)
+    K, N, M = 1024, 4096, 2048
+    w = (torch.randn(K, N, generator=g) * 0.03).bfloat16().float()
+    w[torch.rand(K, N, generator=g) < 0.5] = 0
+    s = S.encode(w.cuda(), value_dtype="bf16")
+    s.compute_format()
+    f = S.fuse([S.AdapterPair((torch.randn(K, 16, generator=g) / 32).bfloat16().float(),
+                              (torch.randn(16, N, generator=g) * 0.03).bfloat16().float(), 16)])
+    wide = torch.randn(M, 2 * K, generator=g).bfloat16().cuda()
+    view = wide[:, K:]
+    y = S.salr_linear(view, s, f)
+    assert torch.equal(y, S.salr_linear(view.contiguous(), s, f))
+    ref = _dense_ref(view.float(), w.cuda(), f)
+    assert float((y.double() - ref.double()).norm() / ref.double().norm()) < 5e-4
