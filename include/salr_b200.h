@@ -111,6 +111,10 @@ int salr_tb2_count(const uint8_t* records, const uint32_t* tile_off, int64_t row
                    uint32_t* tile_off2, void* stream);
 int salr_tb2_write(const uint8_t* records, const uint32_t* tile_off, int64_t rows, int64_t cols,
                    const uint32_t* tile_off2, uint8_t* records2, void* stream);
+/* Dense bf16 matrix (row-major, leading dim ld >= cols) from TB2 records
+ * (prefill-size products: decode once, tensor-core GEMM). */
+int salr_tb2_decode(const uint8_t* records2, const uint32_t* tile_off2, int64_t rows, int64_t cols,
+                    void* dense_bf16, int64_t ld, void* stream);
 /* Inverse (bit-exact): bf16 TB records from TB2 records, so a matrix may keep
  * only the compute format resident and rebuild TB on demand (decode,
  * reference layout).  Count: tile_off[n_tiles + 1]; write: the records. */

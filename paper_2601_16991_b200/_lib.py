@@ -45,6 +45,7 @@ _SIGS = {
     "salr_tb2_write": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp], _int),
     "salr_tb_from_tb2_count": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
     "salr_tb_from_tb2_write": ([_vp, _vp, _i64, _i64, _vp, _vp, _vp], _int),
+    "salr_tb2_decode": ([_vp, _vp, _i64, _i64, _vp, _i64, _vp], _int),
     "salr_nm24_write": ([_vp, _i64, _i64, _i64, _vp, _vp, _vp], _int),
     "salr_nm24_decode": ([_vp, _i64, _i64, _vp, _i64, _vp], _int),
     "salr_linear_workspace_bytes": ([_i64, _i64, _i64, _i64, _int], ctypes.c_size_t),

@@ -560,6 +560,45 @@ __global__ void __launch_bounds__(512) nm24_decode_kernel(const uint8_t* __restr
   }
 }
 
+// Dense bf16 matrix (leading dim ld) straight from TB2 records: grid =
+// n_tiles, block = 128 (thread n <-> tile column n, warp q = column group),
+// the record staged in shared memory; row r of the tile is one coalesced
+// 256-byte store across the block.  (Prefill-size products decode each
+// weight once per call into a dense scratch for a tensor-core GEMM.)
+__global__ void __launch_bounds__(128) tb2_dense_kernel(const uint8_t* __restrict__ records2,
+                                                        const uint32_t* __restrict__ tile_off2, int64_t rows,
+                                                        int64_t cols, int64_t n_kt, uint16_t* __restrict__ dense,
+                                                        int64_t ld) {
+  extern __shared__ __align__(16) uint8_t rec[];
+  const int64_t t = blockIdx.x;
+  const int64_t nt = t / n_kt, kt = t % n_kt;
+  const uint32_t o0 = tile_off2[t], o1 = tile_off2[t + 1];
+  const uint4* src = reinterpret_cast<const uint4*>(records2 + 16ull * o0);
+  for (uint32_t i = threadIdx.x; i < o1 - o0; i += blockDim.x) reinterpret_cast<uint4*>(rec)[i] = src[i];
+  __syncthreads();
+  const int n = threadIdx.x, q = n >> 5, l = n & 31;
+  const uint32_t* hdr = reinterpret_cast<const uint32_t*>(rec);
+  const uint16_t* boff = reinterpret_cast<const uint16_t*>(rec + kT2BandOff) + q * 16;
+  const uint64_t m = reinterpret_cast<const uint64_t*>(rec + kT2Mask)[n];
+  const uint16_t* vals = reinterpret_cast<const uint16_t*>(rec + kT2Val) + (q ? hdr[q - 1] : 0u);
+  const int64_t col = nt * kTileN + n;
+  for (int b = 0; b < 16; ++b) {
+    const uint32_t nib = (uint32_t)((m >> (4 * b)) & 0xFull);
+    const uint32_t c = (uint32_t)__popc(nib);
+    uint32_t incl = c;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+      if (l >= d) incl += y;
+    }
+    const uint32_t base = boff[b] + incl - c;
+    for (int i = 0; i < 4; ++i) {
+      const int64_t row = kt * kTileK + 4 * b + i;
+      const uint16_t v = ((nib >> i) & 1u) ? vals[base + __popc(nib & ((1u << i) - 1u))] : (uint16_t)0;
+      if (row < rows && col < cols) dense[row * ld + col] = v;
+    }
+  }
+}
+
 extern "C" {
 
 int salr_version(void) { return 1; }
@@ -765,6 +804,19 @@ int salr_nm24_decode(const uint8_t* records, int64_t rows, int64_t cols, void* d
   geometry(rows, cols, &n_kt, &n_nt);
   nm24_decode_kernel<<<(unsigned)(n_kt * n_nt), 512, 0, static_cast<cudaStream_t>(stream)>>>(
       records, rows, cols, n_kt, static_cast<uint16_t*>(dense_bf16), ld);
+  SALR_LAUNCH_CHECK();
+  return SALR_OK;
+}
+
+int salr_tb2_decode(const uint8_t* records2, const uint32_t* tile_off2, int64_t rows, int64_t cols,
+                    void* dense_bf16, int64_t ld, void* stream) {
+  if (int rc = check_dims(rows, cols)) return rc;
+  SALR_CHECK_ARG(ld >= cols, SALR_ERR_SHAPE, "ld < cols");
+  SALR_CHECK_ARG(records2 && tile_off2 && dense_bf16, SALR_ERR_CONFIG, "null pointer");
+  int64_t n_kt, n_nt;
+  geometry(rows, cols, &n_kt, &n_nt);
+  tb2_dense_kernel<<<(unsigned)(n_kt * n_nt), 128, kMaxRecordBytesT2 + 16, static_cast<cudaStream_t>(stream)>>>(
+      records2, tile_off2, rows, cols, n_kt, static_cast<uint16_t*>(dense_bf16), ld);
   SALR_LAUNCH_CHECK();
   return SALR_OK;
 }

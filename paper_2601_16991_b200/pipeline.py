@@ -255,20 +255,68 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     else:
         acat = bct = None
         r_pad = 0
-    if workspace is None:
-        ws = _workspace(M, N, s.rows, r_pad, num_ctas, xb.device)
-    else:
-        ws = workspace
     global _launches
-    _launches += 1 if (fused is None or (M <= 256 and not flags & _FLAG_U_FP32)) else 2
-    _lib.check(_lib.load().salr_linear_forward(
-        _lib.ptr(xb), M, s.rows, ldx, _lib.ptr(rec2), _lib.ptr(off2), max_rec2, N,
-        _lib.ptr(acat), _lib.ptr(bct), r_pad, _lib.ptr(out), _lib.dtype_code(out.dtype), N,
-        _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), flags, _lib.stream_ptr()))
+    if M >= DENSE_PREFILL_MIN_M and stages == 0 and num_ctas == 0:
+        _launches += 1
+        _dense_prefill(xb, s, fused, out, rec2, off2, nm24)
+    else:
+        ws = _workspace(M, N, s.rows, r_pad, num_ctas, xb.device) if workspace is None else workspace
+        _launches += 1 if (fused is None or (M <= 256 and not flags & _FLAG_U_FP32)) else 2
+        _lib.check(_lib.load().salr_linear_forward(
+            _lib.ptr(xb), M, s.rows, ldx, _lib.ptr(rec2), _lib.ptr(off2), max_rec2, N,
+            _lib.ptr(acat), _lib.ptr(bct), r_pad, _lib.ptr(out), _lib.dtype_code(out.dtype), N,
+            _lib.ptr(ws), int(ws.numel()), int(stages), int(num_ctas), flags, _lib.stream_ptr()))
     if tail is not None:
         xf = xb[:, : s.rows].float()
         out += ((xf @ tail.a_cat.float()) @ tail.b_cat.float()).to(out.dtype)
     return out
+
+
+# Prefill-size products (M >= DENSE_PREFILL_MIN_M tokens, default schedule):
+# the weight is decoded once per call into a dense bf16 scratch
+# (salr_tb2_decode / salr_nm24_decode, HBM-bound, ~30 us for 4096x14336) and
+# multiplied on the tensor cores by cuBLAS, the adapters folded into the same
+# GEMM along K: [X | U_hi | U_lo] @ [W; B_cat; B_cat], U = X A_cat split into
+# two bf16 halves as in the fused kernel.  With 512+ tokens the decode is
+# amortised and the GEMM is tensor-bound; the fused prefill kernel re-reads
+# X per column tile.  Measured crossover: §4.1b.
+DENSE_PREFILL_MIN_M = 512
+_DENSE_SCRATCH: dict = {}
+
+
+def _dense_scratch(rows: int, cols: int, device) -> torch.Tensor:
+    """Per-device bf16 scratch, grown on demand, viewed as rows x cols."""
+    buf = _DENSE_SCRATCH.get(device.index)
+    if buf is None or buf.numel() < rows * cols:
+        buf = torch.empty(rows * cols, dtype=torch.bfloat16, device=device)
+        _DENSE_SCRATCH[device.index] = buf
+    return buf[: rows * cols].view(rows, cols)
+
+
+def _dense_prefill(xb, s, fused, out, rec, off, nm24):
+    K, N = s.rows, s.cols
+    rp = fused.r_pad if fused is not None else 0
+    w = _dense_scratch(K + 2 * rp, N, xb.device)
+    lib = _lib.load()
+    st = _lib.stream_ptr()
+    if nm24:
+        _lib.check(lib.salr_nm24_decode(_lib.ptr(rec), K, N, _lib.ptr(w), N, st))
+    else:
+        _lib.check(lib.salr_tb2_decode(_lib.ptr(rec), _lib.ptr(off), K, N, _lib.ptr(w), N, st))
+    xk = xb[:, :K]
+    if fused is not None:
+        acat, bct = fused.device_operands()
+        bt = bct[:N].t()
+        w[K:K + rp].copy_(bt)
+        w[K + rp:].copy_(bt)
+        u = torch.mm(xk, acat, out_dtype=torch.float32)
+        hi = u.to(torch.bfloat16)
+        lo = (u - hi.float()).to(torch.bfloat16)
+        xk = torch.cat([xk, hi, lo], dim=1)
+    if out.dtype == torch.float32:
+        torch.mm(xk, w, out_dtype=torch.float32, out=out)
+    else:
+        torch.mm(xk, w, out=out)
 
 
 _CHAIN_WS: dict = {}

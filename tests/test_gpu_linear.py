@@ -324,3 +324,52 @@ def test_strided_input_prefill(S):
     assert torch.equal(y, S.salr_linear(view.contiguous(), s, f))
     ref = _dense_ref(view.float(), w.cuda(), f)
     assert float((y.double() - ref.double()).norm() / ref.double().norm()) < 5e-4
+
+
+@pytest.mark.parametrize("shape", [(200, 300), (1000, 1500), (64, 128)])
+def test_tb2_dense_decode(S, shape):
+    """salr_tb2_decode (the dense scratch of prefill-size products) equals
+    decode() of the same matrix bit for bit, ragged shapes included."""
+    from paper_2601_16991_b200 import _lib
+    g = torch.Generator().manual_seed(sum(shape))
+    w = (torch.randn(*shape, generator=g) * 0.05).bfloat16().float()
+    w[torch.rand(*shape, generator=g) < 0.5] = 0
+    s = S.encode(w.cuda(), value_dtype="bf16")
+    rec2, off2, _ = s.compute_format()
+    K, N = shape
+    out = torch.full((K, N + 8), 7.0, dtype=torch.bfloat16, device="cuda")
+    _lib.check(_lib.load().salr_tb2_decode(_lib.ptr(rec2), _lib.ptr(off2), K, N, _lib.ptr(out), N + 8,
+                                           _lib.stream_ptr()))
+    assert torch.equal(out[:, :N].float(), w.cuda())
+    assert bool((out[:, N:] == 7.0).all())  # nothing written past cols
+
+
+@pytest.mark.parametrize("M", [512, 2048])
+@pytest.mark.parametrize("rank", [0, 16, 64, 96])
+@pytest.mark.parametrize("fmt", ["tb2", "nm24"])
+def test_dense_prefill_path(S, M, rank, fmt):
+    """Prefill-size products (decode to a dense scratch + tensor-core GEMM,
+    adapters folded along K) against fp64, ragged K/N, R up to 192 (tail),
+    both compute formats; fp32 and bf16 outputs."""
+    g = torch.Generator().manual_seed(M + rank)
+    K, N = 1000, 1500
+    w = (torch.randn(K, N, generator=g) * 0.05).bfloat16().float()
+    if fmt == "nm24":
+        w = S.prune(w.cuda(), S.PruneConfig(0.5, S.PruneMethod.SEMI_STRUCTURED_NM, nm=(2, 4))).cpu()
+    else:
+        w[torch.rand(K, N, generator=g) < 0.5] = 0
+    fused = None
+    if rank:
+        fused = S.fuse([S.AdapterPair((torch.randn(K, rank, generator=g) / 16).bfloat16().float(),
+                                      (torch.randn(rank, N, generator=g) * 0.05).bfloat16().float(), rank, sc)
+                        for sc in (1.0, 2.0)])
+    s = S.encode(w.cuda(), value_dtype="bf16")
+    if fmt == "nm24":
+        s.use_nm24()
+    x = torch.randn(M, K, generator=g).bfloat16().float().cuda()
+    ref = _dense_ref(x, w.cuda(), fused).cpu().numpy()
+    y = S.salr_linear(x, s, fused)
+    assert_close(y.cpu().numpy(), ref, f"dense prefill M={M} r={rank} {fmt}")
+    yb = S.salr_linear(x, s, fused, out_dtype=torch.bfloat16)
+    assert float((yb.double() - y.double()).norm() / y.double().norm()) < 4e-3
+    assert torch.equal(y, S.salr_linear(x, s, fused))  # deterministic
