@@ -285,11 +285,14 @@ _DENSE_SCRATCH: dict = {}
 
 
 def _dense_scratch(rows: int, cols: int, device) -> torch.Tensor:
-    """Per-device bf16 scratch, grown on demand, viewed as rows x cols."""
-    buf = _DENSE_SCRATCH.get(device.index)
+    """bf16 scratch per (device, stream) -- calls on one stream are ordered,
+    calls on different streams get their own -- grown on demand, viewed as
+    rows x cols."""
+    key = (device.index, torch.cuda.current_stream(device).cuda_stream)
+    buf = _DENSE_SCRATCH.get(key)
     if buf is None or buf.numel() < rows * cols:
         buf = torch.empty(rows * cols, dtype=torch.bfloat16, device=device)
-        _DENSE_SCRATCH[device.index] = buf
+        _DENSE_SCRATCH[key] = buf
     return buf[: rows * cols].view(rows, cols)
 
 
