@@ -37,7 +37,7 @@ for K, N in ((4096, 4096), (4096, 14336)):
     xs = x.view(M, 8, K // 8).transpose(0, 1)
     as_ = acat.view(8, K // 8, 64)
     t_ubmm = timed(lambda: torch.bmm(xs, as_, out_dtype=torch.float32).sum(0))
-    t_cat = timed(lambda: torch.cat([x, acat[:M].t()[:0].t() if False else x[:, :128]], dim=1))
+    t_cat = timed(lambda: torch.cat([x, x[:, :128]], dim=1))
     xc = uchain()
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     t_mm = timed(lambda: torch.mm(xc, dense, out=out))
