@@ -582,19 +582,43 @@ __global__ void __launch_bounds__(128) tb2_dense_kernel(const uint8_t* __restric
   const uint64_t m = reinterpret_cast<const uint64_t*>(rec + kT2Mask)[n];
   const uint16_t* vals = reinterpret_cast<const uint16_t*>(rec + kT2Val) + (q ? hdr[q - 1] : 0u);
   const int64_t col = nt * kTileN + n;
+  // interior tiles (the common case) skip the per-element bounds checks;
+  // one row pointer walks down the column
+  const int64_t row0 = kt * kTileK;
+  const bool full = row0 + kTileK <= rows && nt * kTileN + kTileN <= cols;
+  const int vrows = full ? kTileK : (col < cols ? (int)(rows - row0 < kTileK ? rows - row0 : kTileK) : 0);
+  uint16_t* p = dense + row0 * ld + col;
+  // the 16 band counts as bytes of 4 words (SWAR nibble popcount), one
+  // byte-lane warp scan per word (counts <= 4, sums <= 128)
+  uint64_t x = m - ((m >> 1) & 0x5555555555555555ull);
+  x = (x & 0x3333333333333333ull) + ((x >> 2) & 0x3333333333333333ull);
+  uint32_t cw[4], ew[4];
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    const uint32_t v = (uint32_t)(x >> (16 * w)) & 0xFFFFu;
+    cw[w] = (v & 0xFu) | ((v & 0xF0u) << 4) | ((v & 0xF00u) << 8) | ((v & 0xF000u) << 12);
+    ew[w] = cw[w];
+  }
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ew[w], d);
+      if (l >= d) ew[w] += y;
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < 4; ++w) ew[w] -= cw[w];
+#pragma unroll
   for (int b = 0; b < 16; ++b) {
     const uint32_t nib = (uint32_t)((m >> (4 * b)) & 0xFull);
-    const uint32_t c = (uint32_t)__popc(nib);
-    uint32_t incl = c;
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-      if (l >= d) incl += y;
-    }
-    const uint32_t base = boff[b] + incl - c;
+    const uint16_t* vp = vals + boff[b] + ((ew[b >> 2] >> (8 * (b & 3))) & 0xFFu);
+#pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int64_t row = kt * kTileK + 4 * b + i;
-      const uint16_t v = ((nib >> i) & 1u) ? vals[base + __popc(nib & ((1u << i) - 1u))] : (uint16_t)0;
-      if (row < rows && col < cols) dense[row * ld + col] = v;
+      uint16_t v = 0;
+      if ((nib >> i) & 1u) v = *vp++;
+      if (4 * b + i < vrows) *p = v;
+      p += ld;
     }
   }
 }
@@ -815,6 +839,16 @@ int salr_tb2_decode(const uint8_t* records2, const uint32_t* tile_off2, int64_t 
   SALR_CHECK_ARG(records2 && tile_off2 && dense_bf16, SALR_ERR_CONFIG, "null pointer");
   int64_t n_kt, n_nt;
   geometry(rows, cols, &n_kt, &n_nt);
+  // one 17.6 KB record slot per 128-thread block: ask for the shared-memory
+  // carve-out that lets ~12 blocks share an SM (the default may leave 1-2)
+  static bool carve[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !carve[dev]) {
+    cudaFuncSetAttribute(tb2_dense_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         (int)cudaSharedmemCarveoutMaxShared);
+    carve[dev] = true;
+  }
   tb2_dense_kernel<<<(unsigned)(n_kt * n_nt), 128, kMaxRecordBytesT2 + 16, static_cast<cudaStream_t>(stream)>>>(
       records2, tile_off2, rows, cols, n_kt, static_cast<uint16_t*>(dense_bf16), ld);
   SALR_LAUNCH_CHECK();
