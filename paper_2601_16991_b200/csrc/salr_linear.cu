@@ -2067,6 +2067,9 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   int64_t ctas = num_ctas > 0 ? num_ctas : std::min<int64_t>(sm_count(), (p.units + kMinUnitsPerCta - 1) / kMinUnitsPerCta);
 // (not for a single token: there the split-K fixup is one row and the
 // extra SMs win -- down at M=1 is 2 us slower on 128 CTAs than on 148)
+#ifndef SALR_ALIGNED_GRID_MAX_UNITS_SMALL_M
+#define SALR_ALIGNED_GRID_MAX_UNITS_SMALL_M 32
+#endif
 #ifndef SALR_ALIGNED_GRID_MIN_M
 #define SALR_ALIGNED_GRID_MIN_M 2
 #endif
@@ -2083,6 +2086,9 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
     for (int64_t c = ctas; c >= (6 * ctas + 6) / 7; --c) {
       const int64_t per = p.units / c;
       const bool even = p.units % c == 0 && (p.n_kt % per == 0 || per % p.n_kt == 0);
+      // below 16 tokens the split-K fixup is cheap: trade SMs for alignment
+      // only for short per-CTA ranges (q|k|v, o: ~16-21 units; not down's 56)
+      if (M < 16 && per > SALR_ALIGNED_GRID_MAX_UNITS_SMALL_M) break;
       if (even || c % tiles == 0) {
         ctas = c;
         break;
