@@ -2065,13 +2065,11 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
   // fixup for a pipeline that never fills.
   constexpr int64_t kMinUnitsPerCta = 6;
   int64_t ctas = num_ctas > 0 ? num_ctas : std::min<int64_t>(sm_count(), (p.units + kMinUnitsPerCta - 1) / kMinUnitsPerCta);
-// (not for a single token: there the split-K fixup is one row and the
-// extra SMs win -- down at M=1 is 2 us slower on 128 CTAs than on 148)
 #ifndef SALR_ALIGNED_GRID_MAX_UNITS_SMALL_M
 #define SALR_ALIGNED_GRID_MAX_UNITS_SMALL_M 32
 #endif
 #ifndef SALR_ALIGNED_GRID_MIN_M
-#define SALR_ALIGNED_GRID_MIN_M 2
+#define SALR_ALIGNED_GRID_MIN_M 1
 #endif
   if (num_ctas <= 0 && M >= SALR_ALIGNED_GRID_MIN_M && !(dbg_env("SALR_NO_ALIGNED_GRID"))) {
     // Prefer a grid (>= 6/7 of the SMs) whose per-CTA unit ranges tile the
@@ -2087,7 +2085,8 @@ int salr_linear_forward(const void* x, int64_t M, int64_t K, int64_t ldx, const 
       const int64_t per = p.units / c;
       const bool even = p.units % c == 0 && (p.n_kt % per == 0 || per % p.n_kt == 0);
       // below 16 tokens the split-K fixup is cheap: trade SMs for alignment
-      // only for short per-CTA ranges (q|k|v, o: ~16-21 units; not down's 56)
+      // only for short per-CTA ranges (q|k|v, o: ~16-21 units; down's 56
+      // units are 2 us slower on 128 CTAs than on 148 at M=1)
       if (M < 16 && per > SALR_ALIGNED_GRID_MAX_UNITS_SMALL_M) break;
       if (even || c % tiles == 0) {
         ctas = c;
