@@ -214,7 +214,8 @@ def reset_launch_count() -> None:
 
 def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *, out: torch.Tensor | None = None,
                 out_dtype: torch.dtype = torch.float32, stages: int = 0, num_ctas: int = 0,
-                check_finite: bool = True, workspace: torch.Tensor | None = None, pdl: bool = False) -> torch.Tensor:
+                check_finite: bool = True, workspace: torch.Tensor | None = None, pdl: bool = False,
+                dense_prefill: bool | None = None) -> torch.Tensor:
     """Launch the fused B200 kernel: ``x @ decode(s) [+ (x @ a_cat) @ b_cat]``.
 
     ``x`` is rounded to bf16 (the compute format); ``s`` is used with bf16
@@ -222,6 +223,9 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     ``pdl=True`` launches as a programmatic dependent of the preceding kernel
     (weight streaming overlaps its tail); only valid when that kernel does not
     read ``out`` and the default alternating workspaces are used.
+    ``dense_prefill``: None (default) takes the decode-to-dense + tensor-core
+    GEMM path from ``DENSE_PREFILL_MIN_M`` tokens on with the default
+    schedule; True / False force it / the fused kernels.
     """
     _lib.require_cuda()
     if not isinstance(s, BitmapSparseMatrix):
@@ -256,7 +260,9 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
         acat = bct = None
         r_pad = 0
     global _launches
-    if M >= DENSE_PREFILL_MIN_M and stages == 0 and num_ctas == 0:
+    if dense_prefill is None:
+        dense_prefill = M >= DENSE_PREFILL_MIN_M and stages == 0 and num_ctas == 0
+    if dense_prefill:
         _launches += 1
         _dense_prefill(xb, s, fused, out, rec2, off2, nm24)
     else:
@@ -272,15 +278,16 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
     return out
 
 
-# Prefill-size products (M >= DENSE_PREFILL_MIN_M tokens, default schedule):
+# Prefill-size products (M > 256 tokens, default schedule):
 # the weight is decoded once per call into a dense bf16 scratch
 # (salr_tb2_decode / salr_nm24_decode, HBM-bound, ~30 us for 4096x14336) and
 # multiplied on the tensor cores by cuBLAS, the adapters folded into the same
 # GEMM along K: [X | U_hi | U_lo] @ [W; B_cat; B_cat], U = X A_cat split into
 # two bf16 halves as in the fused kernel.  With 512+ tokens the decode is
 # amortised and the GEMM is tensor-bound; the fused prefill kernel re-reads
-# X per column tile.  Measured crossover: §4.1b.
-DENSE_PREFILL_MIN_M = 512
+# X per column tile.  Measured: faster than the fused
+# prefill kernel at every M > 256 (the decode-size kernel wins up to 256).
+DENSE_PREFILL_MIN_M = 257
 _DENSE_SCRATCH: dict = {}
 
 

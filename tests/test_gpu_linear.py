@@ -222,7 +222,7 @@ def test_prefill_kernel_ragged(S, rank, out_dtype):
     s = S.encode(w.cuda(), value_dtype="bf16")
     ref = _dense_ref(x, w.cuda(), fused).cpu().numpy()
     dt = torch.float32 if out_dtype == "f32" else torch.bfloat16
-    y = S.salr_linear(x, s, fused, out_dtype=dt)
+    y = S.salr_linear(x, s, fused, out_dtype=dt, dense_prefill=False)
     info = _last_launch()
     assert info["smem"] > 0 and info["groups"] == -1, info  # the prefill kernel ran
     if out_dtype == "f32":
@@ -231,7 +231,7 @@ def test_prefill_kernel_ragged(S, rank, out_dtype):
         yb = y.double().cpu().numpy()
         err = np.abs(yb - ref)
         assert (err <= 2.0 ** -8 * np.abs(ref) + 2e-3 * np.abs(ref).max()).all(), err.max()
-    assert torch.equal(y, S.salr_linear(x, s, fused, out_dtype=dt))
+    assert torch.equal(y, S.salr_linear(x, s, fused, out_dtype=dt, dense_prefill=False))
 
 
 @pytest.mark.parametrize("M", [1, 8, 32])
@@ -308,8 +308,9 @@ def test_strided_input_no_copy(S, M, adapters):
 
 
 def test_strided_input_prefill(S):
-    """A strided bf16 view through the prefill kernel (M=2048): same result
-    as its contiguous copy (the X tensor map carries the row stride)."""
+    """A strided bf16 view through the prefill kernel and the dense prefill
+    path (M=2048): same result as its contiguous copy (the X tensor map /
+    the GEMM carry the row stride)."""
     g = torch.Generator().manual_seed(5)
     K, N, M = 1024, 4096, 2048
     w = (torch.randn(K, N, generator=g) * 0.03).bfloat16().float()
@@ -320,10 +321,11 @@ def test_strided_input_prefill(S):
                               (torch.randn(16, N, generator=g) * 0.03).bfloat16().float(), 16)])
     wide = torch.randn(M, 2 * K, generator=g).bfloat16().cuda()
     view = wide[:, K:]
-    y = S.salr_linear(view, s, f)
-    assert torch.equal(y, S.salr_linear(view.contiguous(), s, f))
     ref = _dense_ref(view.float(), w.cuda(), f)
-    assert float((y.double() - ref.double()).norm() / ref.double().norm()) < 5e-4
+    for dense in (False, True):  # the fused prefill kernel and the dense path
+        y = S.salr_linear(view, s, f, dense_prefill=dense)
+        assert torch.equal(y, S.salr_linear(view.contiguous(), s, f, dense_prefill=dense))
+        assert float((y.double() - ref.double()).norm() / ref.double().norm()) < 5e-4
 
 
 @pytest.mark.parametrize("shape", [(200, 300), (1000, 1500), (64, 128)])
@@ -344,7 +346,7 @@ def test_tb2_dense_decode(S, shape):
     assert bool((out[:, N:] == 7.0).all())  # nothing written past cols
 
 
-@pytest.mark.parametrize("M", [512, 2048])
+@pytest.mark.parametrize("M", [300, 512, 2048])
 @pytest.mark.parametrize("rank", [0, 16, 64, 96])
 @pytest.mark.parametrize("fmt", ["tb2", "nm24"])
 def test_dense_prefill_path(S, M, rank, fmt):

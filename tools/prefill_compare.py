@@ -1,5 +1,5 @@
 """Prefill-size products: fused prefill kernel vs decode-to-dense + cuBLAS
-(the default path from DENSE_PREFILL_MIN_M tokens) vs cuBLAS on the merged
+(the default path above 256 tokens) vs cuBLAS on the merged
 dense weight; graph-timed over rotating weight copies, adapters r16+r16.
 
     python tools/prefill_compare.py [--shapes q,gate,down] [--tokens 256,512,1024,2048]
@@ -60,14 +60,11 @@ for name in a.shapes.split(","):
         x = torch.randn(M, K, device="cuda").bfloat16()
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         res = {"shape": name, "K": K, "N": N, "M": M}
-        for key, thr in (("fused_us", 1 << 30), ("dense_us", 0)):
-            pipeline.DENSE_PREFILL_MIN_M = thr
-
-            def run():
+        for key, dense in (("fused_us", False), ("dense_us", True)):
+            def run(dense=dense):
                 for s in mats:
-                    S.salr_linear(x, s, f, out=out, check_finite=False)
+                    S.salr_linear(x, s, f, out=out, check_finite=False, dense_prefill=dense)
             res[key] = round(timed(run, a.iters) / len(mats), 1)
-        pipeline.DENSE_PREFILL_MIN_M = 512
 
         def blas():
             for w in dense:
