@@ -60,10 +60,10 @@ for name in a.shapes.split(","):
         x = torch.randn(M, K, device="cuda").bfloat16()
         out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
         res = {"shape": name, "K": K, "N": N, "M": M}
-        for key, dense in (("fused_us", False), ("dense_us", True)):
-            def run(dense=dense):
+        for key, use_dense in (("fused_us", False), ("dense_us", True)):
+            def run(use_dense=use_dense):
                 for s in mats:
-                    S.salr_linear(x, s, f, out=out, check_finite=False, dense_prefill=dense)
+                    S.salr_linear(x, s, f, out=out, check_finite=False, dense_prefill=use_dense)
             res[key] = round(timed(run, a.iters) / len(mats), 1)
 
         def blas():
