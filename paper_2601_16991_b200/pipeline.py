@@ -303,26 +303,46 @@ def _dense_scratch(rows: int, cols: int, device) -> torch.Tensor:
     return buf[: rows * cols].view(rows, cols)
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(device) -> torch.cuda.Stream:
+    st = _SIDE_STREAMS.get(device.index)
+    if st is None:
+        st = _SIDE_STREAMS[device.index] = torch.cuda.Stream(device)
+    return st
+
+
 def _dense_prefill(xb, s, fused, out, rec, off, nm24):
     K, N = s.rows, s.cols
     rp = fused.r_pad if fused is not None else 0
     w = _dense_scratch(K + 2 * rp, N, xb.device)
     lib = _lib.load()
+    main = torch.cuda.current_stream(xb.device)
+    xk = xb[:, :K]
+    side = None
+    if fused is not None:
+        # U = X A_cat and the [X | U_hi | U_lo] operand on a side stream,
+        # concurrently with the (HBM-bound) weight decode
+        side = _side_stream(xb.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            acat, bct = fused.device_operands()
+            u = torch.mm(xk, acat, out_dtype=torch.float32)
+            hi = u.to(torch.bfloat16)
+            lo = (u - hi.float()).to(torch.bfloat16)
+            xk = torch.cat([xk, hi, lo], dim=1)
     st = _lib.stream_ptr()
     if nm24:
         _lib.check(lib.salr_nm24_decode(_lib.ptr(rec), K, N, _lib.ptr(w), N, st))
     else:
         _lib.check(lib.salr_tb2_decode(_lib.ptr(rec), _lib.ptr(off), K, N, _lib.ptr(w), N, st))
-    xk = xb[:, :K]
-    if fused is not None:
-        acat, bct = fused.device_operands()
+    if side is not None:
         bt = bct[:N].t()
         w[K:K + rp].copy_(bt)
         w[K + rp:].copy_(bt)
-        u = torch.mm(xk, acat, out_dtype=torch.float32)
-        hi = u.to(torch.bfloat16)
-        lo = (u - hi.float()).to(torch.bfloat16)
-        xk = torch.cat([xk, hi, lo], dim=1)
+        main.wait_stream(side)
+        xk.record_stream(main)
     if out.dtype == torch.float32:
         torch.mm(xk, w, out_dtype=torch.float32, out=out)
     else:
