@@ -261,7 +261,8 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
         r_pad = 0
     global _launches
     if dense_prefill is None:
-        dense_prefill = M >= DENSE_PREFILL_MIN_M and stages == 0 and num_ctas == 0
+        dense_prefill = stages == 0 and num_ctas == 0 and (
+            M >= DENSE_PREFILL_MIN_M or (M > 128 and s.rows * s.cols <= DENSE_SMALL_W_MAX))
     if dense_prefill:
         _launches += 1
         _dense_prefill(xb, s, fused, out, rec2, off2, nm24)
@@ -288,6 +289,11 @@ def salr_linear(x, s: BitmapSparseMatrix, fused: FusedAdapters | None = None, *,
 # X per column tile.  Measured: faster than the fused
 # prefill kernel at every M > 256 (the decode-size kernel wins up to 256).
 DENSE_PREFILL_MIN_M = 257
+# Between 129 and 256 tokens the fused decode-size kernel streams the weight
+# twice (two 128-token chunks): there the dense path wins for weights up to
+# ~32 M entries (q, k, v, o, q|k|v) and loses for the MLP ones
+# (profiles/r02_prefill_compare_midM.jsonl).
+DENSE_SMALL_W_MAX = 32 * 1024 * 1024
 _DENSE_SCRATCH: dict = {}
 
 
